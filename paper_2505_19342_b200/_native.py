@@ -1,0 +1,79 @@
+"""ctypes binding of the C-ABI library (include/astra_b200.h).
+
+There is deliberately no fallback: if the shared object is missing or was
+built for another ABI, every hot-path call raises.  Status codes map to the
+reference's exception taxonomy (seqvq/errors.py:4-33).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .errors import IndexCorruptionError, MaskError, ShapeError
+
+_LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libastra_b200.so"
+ABI_VERSION = 1
+
+_c_int = ctypes.c_int
+_c_ll = ctypes.c_longlong
+_vp = ctypes.c_void_p
+_fp = ctypes.c_void_p  # float*, passed as raw device addresses
+
+# name -> argtypes; every symbol declared in include/astra_b200.h
+SIGNATURES: dict[str, list] = {
+    "astra_last_error": [],
+    "astra_abi_version": [],
+    "astra_gemm": [_vp, _vp, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _fp, _fp,
+                   _c_int, _fp, _c_int, _vp, _vp, _c_int, _c_int, _vp],
+}
+
+_lib = None
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+def lib_path() -> Path:
+    return Path(os.environ.get("ASTRA_B200_LIB", _LIB_PATH))
+
+
+def load():
+    """Load (once) and type the native library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = lib_path()
+    if not path.exists():
+        raise NativeLibraryMissing(
+            f"native library {path} not built; run `python -m paper_2505_19342_b200.build`")
+    lib = ctypes.CDLL(str(path))
+    for name, argtypes in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = ctypes.c_char_p if name == "astra_last_error" else ctypes.c_int
+    if lib.astra_abi_version() != ABI_VERSION:
+        raise NativeLibraryMissing("native library ABI mismatch; rebuild it")
+    _lib = lib
+    return lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == 0:
+        return
+    msg = (_lib.astra_last_error() or b"").decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if status == 1:
+        raise ShapeError(text)
+    if status == 2:
+        raise IndexCorruptionError(text)
+    if status == 5:
+        raise MaskError(text)
+    raise RuntimeError(text)
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args), name)
