@@ -247,6 +247,23 @@ def make_classify_data(dim, tokens, count, seed, spread=0.3, signal_fraction=0.2
     return xs, np.asarray(labels, dtype=np.int64)
 
 
+def make_lm_data(vocab, tokens, count, seed, task_seed=0):
+    """train.py:93-112: Markov-chain id sequences (vocab <= 64)."""
+    gen = generator(seed, "lm-data")
+    logits = 2.0 * generator(task_seed, "lm-chain").normal(size=(vocab, vocab))
+    z = logits - logits.max(axis=1, keepdims=True)
+    p = np.exp(z)
+    p /= p.sum(axis=1, keepdims=True)
+    seqs = []
+    for _ in range(count):
+        ids = np.empty(tokens + 1, dtype=np.int64)
+        ids[0] = int(gen.integers(0, vocab))
+        for t in range(tokens):
+            ids[t + 1] = int(gen.choice(vocab, p=p[ids[t]]))
+        seqs.append(ids)
+    return seqs
+
+
 # -------------------------------------------------------------- cluster.py
 def partition_tokens(tokens: int, devices: int):
     """cluster.py:62-76: contiguous near-even shards, remainder to trailing devices."""
