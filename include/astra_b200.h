@@ -58,6 +58,60 @@ int astra_gemm(const void* a_hi, const void* a_lo, int lda, const void* b_hi, co
                const float* residual, int ld_res, float* out_f32, int ld_f32, void* out_hi,
                void* out_lo, int ld_bf, int gelu, void* stream);
 
+/* ------------------------------------------------------------ VQ encode
+ * Replaces vq.quantize / vq._nearest (vq.py:126-131, :207-222): per group g,
+ * idx = argmin_k ||x_g - c_{g,k}||^2 evaluated in fp64, ties -> lowest k.
+ *
+ * B200 design: the distance GEMM runs on tcgen05 in split bf16x3 (fp32-class)
+ * with a fused per-row argmin epilogue that keeps every code whose approximate
+ * score lies inside a proven error window of the best; a second kernel merges
+ * the code-chunk candidates and re-ranks the (rare) multi-candidate rows in
+ * exact fp64, so the indices are bit-identical to the fp64 reference.
+ */
+typedef struct AstraCodebook {
+  int groups;            /* G                                                */
+  int size;              /* K (codes per group)                              */
+  int group_dim;         /* D/G                                              */
+  int padded_dim;        /* D/G rounded up to 64 (bf16 swizzle row)          */
+  const float* centroids;   /* [G, K, D/G] fp32 (Codebook.centroids, vq.py:31-76) */
+  const void* c_hi;         /* [G, K, padded] bf16 hi split, zero padded      */
+  const void* c_lo;         /* [G, K, padded] bf16 lo split                   */
+  const float* c_sq;        /* [G, K] ||c||^2 (fp32, epilogue score)          */
+  const double* c_sq64;     /* [G, K] ||c||^2 (fp64, exact re-rank)           */
+  const float* c_norm_max;  /* [G] max_k ||c_k||                              */
+} AstraCodebook;
+
+/* Fill the derived tables of `cb` (c_hi, c_lo, c_sq, c_sq64, c_norm_max are
+ * caller-allocated device buffers named in cb; cb->centroids is the input). */
+int astra_vq_prepare(const AstraCodebook* cb, void* stream);
+
+/* Bytes of scratch astra_vq_encode needs for M tokens. */
+int64_t astra_vq_encode_workspace(int M, int groups, int size, int padded_dim);
+
+/* idx_out[m, g] (int32, [M, G] row-major) = nearest code of token row
+ * rows ? rows[m] : m of x (fp32, row pitch ldx).  stats (nullable, int32[4],
+ * accumulated): {tokens re-ranked in fp64, tokens needing a full fp64 scan,
+ * total window candidates, 0}. */
+int astra_vq_encode(const AstraCodebook* cb, const float* x, int M, int ldx, const int32_t* rows,
+                    int32_t* idx_out, int32_t* stats, void* workspace, int64_t workspace_bytes,
+                    void* stream);
+
+/* ------------------------------------------------------------ VQ decode
+ * Replaces vq.dequantize (vq.py:225-233): out[m, g*gd:(g+1)*gd] =
+ * centroids[g][idx[m, g]].  Out-of-range indices are not dereferenced; they
+ * set *err_flag = 1 (caller maps it to IndexCorruptionError). */
+int astra_vq_decode(const AstraCodebook* cb, const int32_t* idx, int M, float* out, int ldo,
+                    int32_t* err_flag, void* stream);
+
+/* ------------------------------------------------------- index wire format
+ * The exchanged payload of allgather_indices (cluster.py:144-160; the
+ * reference only accounts ceil(log2 K) bits per index, vq.py:24-28): an
+ * LSB-first bitstream of `bits`-bit codes in [token, group] order, padded to
+ * whole uint32 words. */
+int astra_pack_indices(const int32_t* idx, int count, int bits, uint32_t* words, void* stream);
+int astra_unpack_indices(const uint32_t* words, int count, int bits, int size, int32_t* idx,
+                         int32_t* err_flag, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,14 @@ SIGNATURES: dict[str, list] = {
     "astra_abi_version": [],
     "astra_gemm": [_vp, _vp, _c_int, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int, _fp, _fp,
                    _c_int, _fp, _c_int, _vp, _vp, _c_int, _c_int, _vp],
+    "astra_vq_prepare": [_vp, _vp],
+    "astra_vq_encode_workspace": [_c_int, _c_int, _c_int, _c_int],
+    "astra_vq_encode": [_vp, _vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_ll, _vp],
+    "astra_vq_decode": [_vp, _vp, _c_int, _vp, _c_int, _vp, _vp],
+    "astra_pack_indices": [_vp, _c_int, _c_int, _vp, _vp],
+    "astra_unpack_indices": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp],
 }
+_RESTYPES = {"astra_last_error": ctypes.c_char_p, "astra_vq_encode_workspace": ctypes.c_longlong}
 
 _lib = None
 
@@ -53,7 +60,7 @@ def load():
     for name, argtypes in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
-        fn.restype = ctypes.c_char_p if name == "astra_last_error" else ctypes.c_int
+        fn.restype = _RESTYPES.get(name, ctypes.c_int)
     if lib.astra_abi_version() != ABI_VERSION:
         raise NativeLibraryMissing("native library ABI mismatch; rebuild it")
     _lib = lib

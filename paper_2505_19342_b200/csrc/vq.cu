@@ -1,0 +1,475 @@
+// VQ encode / decode and the packed-index wire format.
+//
+// Reference: vq._nearest (vq.py:126-131) scores d2 = ||p||^2 - 2 p.c + ||c||^2 in
+// fp64 and takes argmin with ties -> lowest index; vq.quantize (vq.py:207-222)
+// runs it per group; vq.dequantize (vq.py:225-233) gathers centroid rows.
+//
+// Encode on B200 = three kernels:
+//   1. vq_split      fp32 token rows -> bf16 hi/lo split, one zero-padded [M, 64k] slab per
+//                    group, and ||x_g|| (for the error window).
+//   2. tc_gemm<VqEpilogue>  tcgen05 bf16x3 distance GEMM (scores = ||c||^2 - 2 x.c, the
+//                    row-constant ||x||^2 dropped) with a fused per-row argmin epilogue that
+//                    records, per 256-code chunk, the best score and every code inside the
+//                    window best + 2*Delta.
+//   3. vq_finalize   merge the chunks; a row with one surviving candidate is decided; rows
+//                    with several are re-ranked in exact fp64 (reference formula and order);
+//                    a chunk that overflowed its candidate list falls back to a full fp64 scan.
+//
+// Error window.  With x = xh + xl, c = ch + cl (bf16, RN) the computed xh.ch + xh.cl + xl.ch
+// differs from x.c by at most 3.02 * 2^-16 * sum|x_i c_i| <= 3.02 * 2^-16 ||x|| ||c||
+// (Cauchy-Schwarz) plus fp32 accumulation error; kTau = 2^-14 covers the former with 30%
+// headroom left for the latter (measured |err| ~ 1.3e-6 ||x|| ||c||).  Score error is 2x
+// that plus fp32 rounding of the epilogue arithmetic.
+#include "host_common.h"
+#include "tc_gemm.cuh"
+
+namespace astra {
+
+constexpr int kVqBN = 256;
+constexpr int kVqCap = 4;          // candidates recorded per (row, chunk)
+constexpr float kTau = 1.0f / 16384.0f;
+
+struct VqWorkspace {
+  __nv_bfloat16* x_hi;
+  __nv_bfloat16* x_lo;
+  float* x_norm;      // [G, M]
+  float* rec_best;    // [G, M, nchunk]
+  int* rec_cnt;       // [G, M, nchunk]
+  int* rec_idx;       // [G, M, nchunk, cap]
+  float* rec_score;   // [G, M, nchunk, cap]
+};
+
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
+  const int nchunk = (K + kVqBN - 1) / kVqBN;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  size_t o_hi = take((size_t)G * M * gdp * 2);
+  size_t o_lo = take((size_t)G * M * gdp * 2);
+  size_t o_norm = take((size_t)G * M * 4);
+  size_t o_best = take((size_t)G * M * nchunk * 4);
+  size_t o_cnt = take((size_t)G * M * nchunk * 4);
+  size_t o_idx = take((size_t)G * M * nchunk * kVqCap * 4);
+  size_t o_sc = take((size_t)G * M * nchunk * kVqCap * 4);
+  if (w && base) {
+    uint8_t* b = reinterpret_cast<uint8_t*>(base);
+    w->x_hi = reinterpret_cast<__nv_bfloat16*>(b + o_hi);
+    w->x_lo = reinterpret_cast<__nv_bfloat16*>(b + o_lo);
+    w->x_norm = reinterpret_cast<float*>(b + o_norm);
+    w->rec_best = reinterpret_cast<float*>(b + o_best);
+    w->rec_cnt = reinterpret_cast<int*>(b + o_cnt);
+    w->rec_idx = reinterpret_cast<int*>(b + o_idx);
+    w->rec_score = reinterpret_cast<float*>(b + o_sc);
+  }
+  return off;
+}
+
+// Half-width of the score error window for a token of norm xn against codes of norm <= cmax.
+__device__ __forceinline__ float score_delta(float xn, float cmax) {
+  return 2.0f * kTau * xn * cmax + 4.8e-7f * (cmax * cmax + 2.0f * xn * cmax) + 1e-30f;
+}
+
+// ------------------------------------------------------------ prepare
+__global__ void vq_prepare_kernel(AstraCodebook cb) {
+  // one warp per (g, k) code row
+  const int warps = (blockDim.x >> 5);
+  const int code = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int G = cb.groups, K = cb.size, gd = cb.group_dim, gdp = cb.padded_dim;
+  if (code >= G * K) return;
+  const float* c = cb.centroids + (size_t)code * gd;
+  __nv_bfloat16* hi = (__nv_bfloat16*)cb.c_hi + (size_t)code * gdp;
+  __nv_bfloat16* lo = (__nv_bfloat16*)cb.c_lo + (size_t)code * gdp;
+  double s64 = 0.0;
+  for (int e = lane; e < gdp; e += 32) {
+    float v = e < gd ? c[e] : 0.0f;
+    __nv_bfloat16 h, l;
+    split_bf16(v, h, l);
+    hi[e] = h;
+    lo[e] = l;
+    s64 += (double)v * (double)v;
+  }
+  for (int o = 16; o; o >>= 1) s64 += __shfl_xor_sync(0xffffffffu, s64, o);
+  if (lane == 0) {
+    ((double*)cb.c_sq64)[code] = s64;
+    ((float*)cb.c_sq)[code] = (float)s64;
+  }
+}
+
+__global__ void vq_normmax_kernel(AstraCodebook cb) {
+  const int g = blockIdx.x;
+  float m = 0.f;
+  for (int k = threadIdx.x; k < cb.size; k += blockDim.x)
+    m = fmaxf(m, sqrtf((float)cb.c_sq64[(size_t)g * cb.size + k]));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = fmaxf(r, red[i]);
+    // round up a hair so the window bound stays an upper bound
+    ((float*)cb.c_norm_max)[g] = r * (1.0f + 1e-6f);
+  }
+}
+
+// -------------------------------------------------------------- split
+// one warp per token row: gather, split to bf16 hi/lo per group (zero padded), ||x_g||.
+__global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
+                                const int32_t* __restrict__ rows, int G, int gd, int gdp,
+                                VqWorkspace w) {
+  const int warps = blockDim.x >> 5;
+  const int r = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= M) return;
+  const int src = rows ? rows[r] : r;
+  const float* xr = x + (size_t)src * ldx;
+  for (int g = 0; g < G; ++g) {
+    __nv_bfloat16* hi = w.x_hi + ((size_t)g * M + r) * gdp;
+    __nv_bfloat16* lo = w.x_lo + ((size_t)g * M + r) * gdp;
+    float ss = 0.f;
+    for (int e = lane; e < gdp; e += 32) {
+      float v = e < gd ? __ldg(xr + g * gd + e) : 0.0f;
+      __nv_bfloat16 h, l;
+      split_bf16(v, h, l);
+      hi[e] = h;
+      lo[e] = l;
+      ss = fmaf(v, v, ss);
+    }
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) w.x_norm[(size_t)g * M + r] = sqrtf(ss) * (1.0f + 1e-6f);
+  }
+}
+
+// ---------------------------------------------------------- epilogue
+struct VqEpilogue {
+  int M, K, nchunk;
+  const float* c_sq;        // [G, K]
+  const float* c_norm_max;  // [G]
+  VqWorkspace w;
+
+  __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile,
+                                             uint32_t taddr) const {
+    const int row = tc.m_blk * kBM + row_in_tile;
+    const bool ok = row < M;
+    const int g = tc.batch;
+    const int col_base = tc.n_blk * kVqBN;
+    const float* csq = c_sq + (size_t)g * K;
+    float best = INFINITY;
+    int bidx = -1;
+#pragma unroll 1
+    for (int c0 = 0; c0 < kVqBN; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c0, r);
+      tmem_ld_wait();
+      const int col0 = col_base + c0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = col0 + j;
+        if (col < K) {
+          const float s = fmaf(-2.0f, __uint_as_float(r[j]), __ldg(csq + col));
+          if (s < best) {
+            best = s;
+            bidx = col;
+          }
+        }
+      }
+    }
+    const float xn = ok ? w.x_norm[(size_t)g * M + row] : 0.f;
+    const float thr = best + 2.0f * score_delta(xn, __ldg(c_norm_max + g));
+    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk;
+    int cnt = 0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < kVqBN; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c0, r);
+      tmem_ld_wait();
+      const int col0 = col_base + c0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = col0 + j;
+        if (col < K) {
+          const float s = fmaf(-2.0f, __uint_as_float(r[j]), __ldg(csq + col));
+          if (s <= thr) {
+            if (ok && cnt < kVqCap) {
+              w.rec_idx[rec * kVqCap + cnt] = col;
+              w.rec_score[rec * kVqCap + cnt] = s;
+            }
+            ++cnt;
+          }
+        }
+      }
+    }
+    if (ok) {
+      w.rec_best[rec] = best;
+      w.rec_cnt[rec] = cnt;
+    }
+    (void)bidx;
+  }
+};
+
+// ---------------------------------------------------------- finalize
+__device__ __forceinline__ double warp_sum_d(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// exact reference distance (vq.py:130 evaluation order): (pp - 2 pc) + cc, fp64
+__device__ __forceinline__ double exact_d2(const float* xr, const float* c, int gd, double pp,
+                                           double cc, int lane) {
+  double pc = 0.0;
+  for (int e = lane; e < gd; e += 32) pc = fma((double)__ldg(xr + e), (double)__ldg(c + e), pc);
+  pc = warp_sum_d(pc);
+  return (pp - 2.0 * pc) + cc;
+}
+
+// one warp per (g, row)
+__global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x, int M, int ldx,
+                                   const int32_t* __restrict__ rows, VqWorkspace w, int nchunk,
+                                   int32_t* __restrict__ idx_out, int32_t* __restrict__ stats) {
+  const int warps = blockDim.x >> 5;
+  const int item = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int G = cb.groups, K = cb.size, gd = cb.group_dim;
+  if (item >= G * M) return;
+  const int g = item / M, row = item % M;
+  const size_t rec0 = ((size_t)g * M + row) * nchunk;
+  float best = INFINITY;
+  for (int c = 0; c < nchunk; ++c) best = fminf(best, w.rec_best[rec0 + c]);
+  const float thr = best + 2.0f * score_delta(w.x_norm[(size_t)g * M + row], cb.c_norm_max[g]);
+  int n = 0, only = -1;
+  bool overflow = false;
+  for (int c = 0; c < nchunk; ++c) {
+    const int cnt = w.rec_cnt[rec0 + c];
+    if (w.rec_best[rec0 + c] > thr) continue;
+    if (cnt > kVqCap) overflow = true;
+    const int m = cnt < kVqCap ? cnt : kVqCap;
+    for (int i = 0; i < m; ++i)
+      if (w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
+        ++n;
+        only = w.rec_idx[(rec0 + c) * kVqCap + i];
+      }
+  }
+  int result = only;
+  if (overflow || n > 1) {
+    const int src = rows ? rows[row] : row;
+    const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
+    double pp = 0.0;
+    for (int e = lane; e < gd; e += 32) pp = fma((double)__ldg(xr + e), (double)__ldg(xr + e), pp);
+    pp = warp_sum_d(pp);
+    const float* cents = cb.centroids + (size_t)g * K * gd;
+    const double* cc = cb.c_sq64 + (size_t)g * K;
+    double bd = INFINITY;
+    int bi = -1;
+    if (overflow) {
+      for (int k = 0; k < K; ++k) {
+        const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
+        if (d < bd) {
+          bd = d;
+          bi = k;
+        }
+      }
+    } else {
+      // candidates arrive in increasing code order (chunks ascending, columns ascending)
+      for (int c = 0; c < nchunk; ++c) {
+        if (w.rec_best[rec0 + c] > thr) continue;
+        const int m = w.rec_cnt[rec0 + c];
+        for (int i = 0; i < m; ++i) {
+          if (w.rec_score[(rec0 + c) * kVqCap + i] > thr) continue;
+          const int k = w.rec_idx[(rec0 + c) * kVqCap + i];
+          const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
+          if (d < bd || (d == bd && k < bi)) {
+            bd = d;
+            bi = k;
+          }
+        }
+      }
+    }
+    result = bi;
+    if (stats && lane == 0) {
+      atomicAdd(&stats[overflow ? 1 : 0], 1);
+    }
+  }
+  if (lane == 0) {
+    idx_out[(size_t)row * G + g] = result;
+    if (stats) atomicAdd(&stats[2], n);
+  }
+}
+
+// ------------------------------------------------------------ decode
+// out[m, g*gd + e] = centroids[g][idx[m, g]][e]; one warp per (m, g), float4 when aligned.
+__global__ void vq_decode_kernel(AstraCodebook cb, const int32_t* __restrict__ idx, int M,
+                                 float* __restrict__ out, int ldo, int32_t* err) {
+  const int warps = blockDim.x >> 5;
+  const int item = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int G = cb.groups, K = cb.size, gd = cb.group_dim;
+  if (item >= M * G) return;
+  const int m = item / G, g = item % G;
+  const int k = __ldg(idx + item);
+  float* o = out + (size_t)m * ldo + (size_t)g * gd;
+  if (k < 0 || k >= K) {
+    if (lane == 0) atomicExch(err, 1);
+    for (int e = lane; e < gd; e += 32) o[e] = 0.f;
+    return;
+  }
+  const float* c = cb.centroids + ((size_t)g * K + k) * gd;
+  if ((gd & 3) == 0 && ((reinterpret_cast<uintptr_t>(o) | reinterpret_cast<uintptr_t>(c)) & 15) == 0) {
+    for (int e = lane * 4; e < gd; e += 128)
+      *reinterpret_cast<float4*>(o + e) = __ldg(reinterpret_cast<const float4*>(c + e));
+  } else {
+    for (int e = lane; e < gd; e += 32) o[e] = __ldg(c + e);
+  }
+}
+
+// ------------------------------------------------------------ packing
+__global__ void pack_kernel(const int32_t* __restrict__ idx, int count, int bits,
+                            uint32_t* __restrict__ words, int nwords) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nwords) return;
+  const long long b0 = (long long)w * 32, b1 = b0 + 32;
+  uint32_t acc = 0;
+  if (bits > 0) {
+    long long first = b0 / bits, last = (b1 - 1) / bits;
+    for (long long i = first; i <= last && i < count; ++i) {
+      const uint64_t v = (uint64_t)(uint32_t)idx[i] & ((1ull << bits) - 1);
+      const long long pos = i * bits - b0;  // may be negative
+      acc |= (uint32_t)(pos >= 0 ? (v << pos) : (v >> (-pos)));
+    }
+  }
+  words[w] = acc;
+}
+
+__global__ void unpack_kernel(const uint32_t* __restrict__ words, int count, int bits, int K,
+                              int32_t* __restrict__ idx, int32_t* err) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint32_t v = 0;
+  if (bits > 0) {
+    const long long b = (long long)i * bits;
+    const int w = (int)(b >> 5), off = (int)(b & 31);
+    uint64_t pair = words[w];
+    if (off + bits > 32) pair |= (uint64_t)words[w + 1] << 32;
+    v = (uint32_t)((pair >> off) & ((1ull << bits) - 1));
+  }
+  if ((int)v >= K) {
+    atomicExch(err, 1);
+    v = 0;
+  }
+  idx[i] = (int32_t)v;
+}
+
+}  // namespace astra
+
+using namespace astra;
+
+extern "C" int astra_vq_prepare(const AstraCodebook* cbp, void* stream) {
+  ASTRA_REQUIRE(cbp, ASTRA_ERR_SHAPE, "null codebook");
+  AstraCodebook cb = *cbp;
+  ASTRA_REQUIRE(cb.groups >= 1 && cb.size >= 1 && cb.group_dim >= 1, ASTRA_ERR_SHAPE,
+                "bad codebook shape");
+  ASTRA_REQUIRE(cb.padded_dim % 64 == 0 && cb.padded_dim >= cb.group_dim, ASTRA_ERR_SHAPE,
+                "padded_dim must be a multiple of 64 >= group_dim");
+  cudaStream_t s = as_stream(stream);
+  const int rows = cb.groups * cb.size;
+  vq_prepare_kernel<<<(rows + 7) / 8, 256, 0, s>>>(cb);
+  vq_normmax_kernel<<<cb.groups, 256, 0, s>>>(cb);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int64_t astra_vq_encode_workspace(int M, int groups, int size, int padded_dim) {
+  return (int64_t)carve(nullptr, nullptr, M, groups, size, padded_dim);
+}
+
+extern "C" int astra_vq_encode(const AstraCodebook* cbp, const float* x, int M, int ldx,
+                               const int32_t* rows, int32_t* idx_out, int32_t* stats,
+                               void* workspace, int64_t workspace_bytes, void* stream) {
+  ASTRA_REQUIRE(cbp && x && idx_out, ASTRA_ERR_SHAPE, "astra_vq_encode: null argument");
+  const AstraCodebook cb = *cbp;
+  ASTRA_REQUIRE(M >= 0, ASTRA_ERR_SHAPE, "astra_vq_encode: M < 0");
+  if (M == 0) return ASTRA_OK;
+  ASTRA_REQUIRE(ldx >= cb.groups * cb.group_dim, ASTRA_ERR_SHAPE, "astra_vq_encode: ldx too small");
+  const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
+  const size_t need = carve(nullptr, nullptr, M, G, K, gdp);
+  ASTRA_REQUIRE((size_t)workspace_bytes >= need, ASTRA_ERR_SHAPE,
+                "astra_vq_encode: workspace %lld < %zu bytes", (long long)workspace_bytes, need);
+  VqWorkspace w;
+  carve(&w, workspace, M, G, K, gdp);
+  cudaStream_t s = as_stream(stream);
+  const int nchunk = (K + kVqBN - 1) / kVqBN;
+
+  vq_split_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, M, ldx, rows, G, cb.group_dim, gdp, w);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+
+  CUtensorMap ta, talo, tb, tblo;
+  int st;
+  if ((st = make_tmap_2d(&ta, w.x_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * M, gdp,
+                         gdp, kBM, kBK, true)))
+    return st;
+  if ((st = make_tmap_2d(&talo, w.x_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * M, gdp,
+                         gdp, kBM, kBK, true)))
+    return st;
+  if ((st = make_tmap_2d(&tb, cb.c_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
+                         gdp, kVqBN, kBK, true)))
+    return st;
+  if ((st = make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
+                         gdp, kVqBN, kBK, true)))
+    return st;
+  VqEpilogue epi{M, K, nchunk, cb.c_sq, cb.c_norm_max, w};
+  auto kern = tc_gemm_kernel<kVqBN, 3, 2, VqEpilogue>;
+  constexpr int smem = gemm_smem_bytes<kVqBN, 3, 2>();
+  static bool configured = false;
+  if (!configured) {
+    ASTRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  TileSched sched{(M + kBM - 1) / kBM, nchunk, G};
+  const int tiles = sched.num_m * sched.num_n * sched.num_b;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, kGemmThreads, smem, s>>>(ta, talo, tb, tblo, gdp, sched, M, K, epi);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+
+  const int items = G * M;
+  vq_finalize_kernel<<<(items + 7) / 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
+                                                      stats);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_vq_decode(const AstraCodebook* cbp, const int32_t* idx, int M, float* out,
+                               int ldo, int32_t* err_flag, void* stream) {
+  ASTRA_REQUIRE(cbp && idx && out && err_flag, ASTRA_ERR_SHAPE, "astra_vq_decode: null argument");
+  const AstraCodebook cb = *cbp;
+  ASTRA_REQUIRE(ldo >= cb.groups * cb.group_dim, ASTRA_ERR_SHAPE, "astra_vq_decode: ldo too small");
+  if (M == 0) return ASTRA_OK;
+  const int items = M * cb.groups;
+  vq_decode_kernel<<<(items + 7) / 8, 256, 0, as_stream(stream)>>>(cb, idx, M, out, ldo, err_flag);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_pack_indices(const int32_t* idx, int count, int bits, uint32_t* words,
+                                  void* stream) {
+  ASTRA_REQUIRE(bits >= 0 && bits <= 31, ASTRA_ERR_SHAPE, "pack: bits out of range");
+  const int nwords = (int)(((long long)count * bits + 31) / 32);
+  if (nwords == 0) return ASTRA_OK;
+  pack_kernel<<<(nwords + 255) / 256, 256, 0, as_stream(stream)>>>(idx, count, bits, words, nwords);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_unpack_indices(const uint32_t* words, int count, int bits, int size,
+                                    int32_t* idx, int32_t* err_flag, void* stream) {
+  ASTRA_REQUIRE(bits >= 0 && bits <= 31, ASTRA_ERR_SHAPE, "unpack: bits out of range");
+  if (count == 0) return ASTRA_OK;
+  unpack_kernel<<<(count + 255) / 256, 256, 0, as_stream(stream)>>>(words, count, bits, size, idx,
+                                                                    err_flag);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}

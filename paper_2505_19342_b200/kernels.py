@@ -66,3 +66,28 @@ def gemm(a_hi: torch.Tensor, b_hi: torch.Tensor, *, a_lo: torch.Tensor | None = 
     _native.call("astra_gemm", _ptr(a_hi), _ptr(a_lo), a_hi.stride(0), _ptr(b_hi), _ptr(b_lo),
                  b_hi.stride(0), M, N, K, passes, _ptr(bias), _ptr(residual), ld_res,
                  _ptr(out_f32), ld_f32, _ptr(out_hi), _ptr(out_lo), ld_bf, int(gelu), _stream())
+
+
+def pack_indices(idx: torch.Tensor, bits: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    """int32 codes -> LSB-first ``bits``-bit stream in uint32 words (astra_pack_indices)."""
+    _require_cuda(idx)
+    idx = idx.contiguous()
+    n = idx.numel()
+    nwords = (n * bits + 31) // 32
+    if out is None:
+        out = torch.empty(nwords, dtype=torch.int32, device=idx.device)
+    _native.call("astra_pack_indices", idx.data_ptr(), n, bits, out.data_ptr(), _stream())
+    return out
+
+
+def unpack_indices(words: torch.Tensor, count: int, bits: int, size: int,
+                   out: torch.Tensor | None = None, err: torch.Tensor | None = None) -> torch.Tensor:
+    """Inverse of pack_indices; codes >= size set *err (IndexCorruptionError upstream)."""
+    _require_cuda(words)
+    if out is None:
+        out = torch.empty(count, dtype=torch.int32, device=words.device)
+    if err is None:
+        err = torch.zeros(1, dtype=torch.int32, device=words.device)
+    _native.call("astra_unpack_indices", words.data_ptr(), count, bits, size, out.data_ptr(),
+                 err.data_ptr(), _stream())
+    return out
