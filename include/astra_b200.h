@@ -112,6 +112,47 @@ int astra_pack_indices(const int32_t* idx, int count, int bits, uint32_t* words,
 int astra_unpack_indices(const uint32_t* words, int count, int bits, int size, int32_t* idx,
                          int32_t* err_flag, void* stream);
 
+/* ---------------------------------------------------------- block ops
+ * tensor.layer_norm (tensor.py:318-345): fp32 row statistics, eps, affine;
+ * writes fp32 and/or the bf16 (hi[, lo]) operand of the following GEMM. */
+int astra_layernorm(const float* x, int M, int D, int ldx, const float* gain, const float* bias,
+                    float eps, float* out_f32, int ld_f32, void* out_hi, void* out_lo, int ld_bf,
+                    void* stream);
+
+/* Stack assembly: embed_classifier_inputs (model.py:275-280) + replica rows
+ * (cluster.py:189-194, :259-262).  row_src[r] >= 0: out[r] = x[row_src[r]] +
+ * pos[row_pos[r]];  row_src[r] < 0: out[r] = cls. */
+int astra_embed_stack(const float* x, const float* pos, const float* cls, const int32_t* row_src,
+                      const int32_t* row_pos, int rows, int D, float* out, void* stream);
+
+/* aggregate_class_tokens / mean_rows (model.py:268-272, tensor.py:200-208):
+ * reps [N, B, D] in device order -> out [B, D], summed in device order then / N. */
+int astra_replica_mean(const float* reps, int N, int B, int D, float* out, void* stream);
+
+/* out[r, :D] = src[idx[r], :D] (row gather, 16-byte vectors). */
+int astra_gather_rows(const float* src, int lds, const int32_t* idx, int rows, int D, float* out,
+                      int ldo, void* stream);
+
+/* Per-layer key map (x_view assembly, cluster.py:182-187): key_map[j] >= 0 is a
+ * local key row; < 0 names remote content token t = -(key_map[j]+1), whose key
+ * becomes remote row codes[t] (G = 1, codebook K/V table) or t (codes == NULL). */
+int astra_key_map(const int32_t* key_map, int n, const int32_t* codes, int32_t* key_src,
+                  void* stream);
+
+/* --------------------------------------------------- mixed-precision attention
+ * attention.multihead_attention + tensor.masked_softmax (attention.py:50-73,
+ * tensor.py:295-315) over each device's mixed key set (cluster.py:201-212).
+ * segs[S, 6] = {q0, nq, qpos0, ncontent, k0, nk} per (device, image) segment;
+ * key_src (see astra_key_map) picks local or remote K/V rows; key_pos is the
+ * global token position (-1 = class replica key); visible iff !causal ||
+ * key_pos <= query_pos.  head_dim must be 64.  in_bf16 selects bf16 inputs. */
+int astra_attention(const void* q, int ldq, const void* k_local, const void* v_local, int ld_local,
+                    const void* k_remote, const void* v_remote, int ld_remote,
+                    const int32_t* key_src, const int32_t* key_pos, const int32_t* segs,
+                    int num_segs, int max_nq, int heads, int head_dim, int causal, int in_bf16,
+                    float scale, float* out_f32, void* out_hi, void* out_lo, int ld_out,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,15 @@ SIGNATURES: dict[str, list] = {
     "astra_vq_decode": [_vp, _vp, _c_int, _vp, _c_int, _vp, _vp],
     "astra_pack_indices": [_vp, _c_int, _c_int, _vp, _vp],
     "astra_unpack_indices": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp],
+    "astra_layernorm": [_vp, _c_int, _c_int, _c_int, _vp, _vp, ctypes.c_float, _vp, _c_int, _vp,
+                        _vp, _c_int, _vp],
+    "astra_embed_stack": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _vp],
+    "astra_replica_mean": [_vp, _c_int, _c_int, _c_int, _vp, _vp],
+    "astra_gather_rows": [_vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp],
+    "astra_key_map": [_vp, _c_int, _vp, _vp, _vp],
+    "astra_attention": [_vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int,
+                        _c_int, _c_int, _c_int, _c_int, _c_int, ctypes.c_float, _vp, _vp, _vp,
+                        _c_int, _vp],
 }
 _RESTYPES = {"astra_last_error": ctypes.c_char_p, "astra_vq_encode_workspace": ctypes.c_longlong}
 

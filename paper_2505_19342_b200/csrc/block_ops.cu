@@ -1,0 +1,241 @@
+// Row-wise block operations of the Astra layer that are HBM-bound:
+//   - LayerNorm (tensor.layer_norm, tensor.py:318-345) producing the next GEMM's operand
+//     (bf16, or the bf16 hi/lo split in parity mode), optionally fp32;
+//   - stack assembly x + pos / class replicas (model.py:275-280, cluster.py:189-194, :259-262);
+//   - replica merge mean (cluster.py:290-292 -> tensor.mean_rows, tensor.py:200-208);
+//   - per-layer key map (G=1 remote keys -> codebook K/V table rows, cluster.py:182-187).
+// One warp per row, 16-byte vector accesses; grids sized in multiples of the SM count.
+#include "host_common.h"
+#include "ptx.cuh"
+
+namespace astra {
+
+// ---------------------------------------------------------------- LayerNorm
+// mean, biased variance, 1/sqrt(var + eps), affine — all fp32 like the reference.
+template <int VPL>  // float4 vectors per lane (D = VPL * 128)
+__global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
+                                 const float* __restrict__ gain, const float* __restrict__ bias,
+                                 float eps, float* __restrict__ out_f32, int ld_f32,
+                                 __nv_bfloat16* __restrict__ out_hi, __nv_bfloat16* __restrict__ out_lo,
+                                 int ld_bf) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < M; row += gridDim.x * warps) {
+    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * ldx);
+    float4 v[VPL];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      v[i] = __ldg(xr + lane + 32 * i);
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float D = (float)(VPL * 128);
+    const float mu = s / D;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      v[i].x -= mu; v[i].y -= mu; v[i].z -= mu; v[i].w -= mu;
+      q += (v[i].x * v[i].x + v[i].y * v[i].y) + (v[i].z * v[i].z + v[i].w * v[i].w);
+    }
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float inv = 1.0f / sqrtf(q / D + eps);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = (lane + 32 * i) * 4;
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c));
+      float4 y;
+      y.x = __fadd_rn(__fmul_rn(__fmul_rn(v[i].x, inv), g.x), b.x);
+      y.y = __fadd_rn(__fmul_rn(__fmul_rn(v[i].y, inv), g.y), b.y);
+      y.z = __fadd_rn(__fmul_rn(__fmul_rn(v[i].z, inv), g.z), b.z);
+      y.w = __fadd_rn(__fmul_rn(__fmul_rn(v[i].w, inv), g.w), b.w);
+      if (out_f32) *reinterpret_cast<float4*>(out_f32 + (size_t)row * ld_f32 + c) = y;
+      if (out_hi) {
+        __nv_bfloat16 h[4], l[4];
+        split_bf16(y.x, h[0], l[0]);
+        split_bf16(y.y, h[1], l[1]);
+        split_bf16(y.z, h[2], l[2]);
+        split_bf16(y.w, h[3], l[3]);
+        *reinterpret_cast<uint2*>(out_hi + (size_t)row * ld_bf + c) = *reinterpret_cast<uint2*>(h);
+        if (out_lo)
+          *reinterpret_cast<uint2*>(out_lo + (size_t)row * ld_bf + c) = *reinterpret_cast<uint2*>(l);
+      }
+    }
+  }
+}
+
+// generic-width fallback (D % 4 == 0 but not a multiple of 128)
+__global__ void layernorm_generic_kernel(const float* __restrict__ x, int M, int D, int ldx,
+                                         const float* __restrict__ gain,
+                                         const float* __restrict__ bias, float eps,
+                                         float* __restrict__ out_f32, int ld_f32,
+                                         __nv_bfloat16* __restrict__ out_hi,
+                                         __nv_bfloat16* __restrict__ out_lo, int ld_bf) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < M; row += gridDim.x * warps) {
+    const float* xr = x + (size_t)row * ldx;
+    float s = 0.f;
+    for (int c = lane; c < D; c += 32) s += xr[c];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mu = s / (float)D;
+    float q = 0.f;
+    for (int c = lane; c < D; c += 32) {
+      const float d = xr[c] - mu;
+      q += d * d;
+    }
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float inv = 1.0f / sqrtf(q / (float)D + eps);
+    for (int c = lane; c < D; c += 32) {
+      const float y = __fadd_rn(__fmul_rn(__fmul_rn(xr[c] - mu, inv), gain[c]), bias[c]);
+      if (out_f32) out_f32[(size_t)row * ld_f32 + c] = y;
+      if (out_hi) {
+        __nv_bfloat16 h, l;
+        split_bf16(y, h, l);
+        out_hi[(size_t)row * ld_bf + c] = h;
+        if (out_lo) out_lo[(size_t)row * ld_bf + c] = l;
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------- stack build
+// row_src[r] >= 0 : content row = x[row_src[r]] + pos[row_pos[r]]   (x is [B*T, D])
+// row_src[r] <  0 : class replica = cls
+__global__ void embed_stack_kernel(const float* __restrict__ x, const float* __restrict__ pos,
+                                   const float* __restrict__ cls, const int32_t* __restrict__ row_src,
+                                   const int32_t* __restrict__ row_pos, int rows, int D,
+                                   float* __restrict__ out) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
+    const int src = row_src[r];
+    float* o = out + (size_t)r * D;
+    if (src >= 0) {
+      const float* a = x + (size_t)src * D;
+      const float* p = pos + (size_t)row_pos[r] * D;
+      for (int c = lane * 4; c < D; c += 128) {
+        float4 va = __ldg(reinterpret_cast<const float4*>(a + c));
+        float4 vp = __ldg(reinterpret_cast<const float4*>(p + c));
+        *reinterpret_cast<float4*>(o + c) =
+            make_float4(va.x + vp.x, va.y + vp.y, va.z + vp.z, va.w + vp.w);
+      }
+    } else {
+      for (int c = lane * 4; c < D; c += 128)
+        *reinterpret_cast<float4*>(o + c) = __ldg(reinterpret_cast<const float4*>(cls + c));
+    }
+  }
+}
+
+// ------------------------------------------------------------- replica mean
+// reps: [N, B, D] in device order -> out [B, D] = (((r0 + r1) + r2) + ...) / N
+__global__ void replica_mean_kernel(const float* __restrict__ reps, int N, int BD,
+                                    float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= BD) return;
+  float s = reps[i];
+  for (int n = 1; n < N; ++n) s += reps[(size_t)n * BD + i];
+  out[i] = s / (float)N;
+}
+
+// gather rows: out[r] = src[idx[r]]   (D floats, float4)
+__global__ void gather_rows_kernel(const float* __restrict__ src, int lds,
+                                   const int32_t* __restrict__ idx, int rows, int D,
+                                   float* __restrict__ out, int ldo) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
+    const float* s = src + (size_t)idx[r] * lds;
+    float* o = out + (size_t)r * ldo;
+    for (int c = lane * 4; c < D; c += 128)
+      *reinterpret_cast<float4*>(o + c) = __ldg(reinterpret_cast<const float4*>(s + c));
+  }
+}
+
+// ------------------------------------------------------------------ key map
+// key_map[j] >= 0 : local key row (copied)
+// key_map[j] <  0 : remote content token t = -(key_map[j]+1); key_src[j] = -(codes[t]+1)
+//                   (G = 1: the K/V table row of its code)  or  -(t+1) when codes == NULL
+__global__ void key_map_kernel(const int32_t* __restrict__ key_map, int n,
+                               const int32_t* __restrict__ codes, int32_t* __restrict__ key_src) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int m = key_map[j];
+  key_src[j] = (m >= 0 || codes == nullptr) ? m : -(codes[-(m + 1)] + 1);
+}
+
+static int grid_rows(int rows, int warps_per_block) {
+  int g = (rows + warps_per_block - 1) / warps_per_block;
+  const int cap = num_sms() * 8;
+  return g < cap ? (g > 0 ? g : 1) : cap;
+}
+
+}  // namespace astra
+
+using namespace astra;
+
+extern "C" int astra_layernorm(const float* x, int M, int D, int ldx, const float* gain,
+                               const float* bias, float eps, float* out_f32, int ld_f32,
+                               void* out_hi, void* out_lo, int ld_bf, void* stream) {
+  ASTRA_REQUIRE(M >= 0 && D > 0, ASTRA_ERR_SHAPE, "layernorm: bad shape");
+  ASTRA_REQUIRE(eps > 0.f, ASTRA_ERR_SHAPE, "layer_norm: eps must be positive");
+  if (M == 0) return ASTRA_OK;
+  cudaStream_t s = as_stream(stream);
+  auto hi = reinterpret_cast<__nv_bfloat16*>(out_hi);
+  auto lo = reinterpret_cast<__nv_bfloat16*>(out_lo);
+  const bool vec = (D % 128 == 0) && (ldx % 4 == 0) && (!out_f32 || ld_f32 % 4 == 0) &&
+                   (!out_hi || ld_bf % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  const int grid = grid_rows(M, 8);
+  if (vec && D == 768)
+    layernorm_kernel<6><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo, ld_bf);
+  else if (vec && D == 1024)
+    layernorm_kernel<8><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo, ld_bf);
+  else if (vec && D == 512)
+    layernorm_kernel<4><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo, ld_bf);
+  else
+    layernorm_generic_kernel<<<grid, 256, 0, s>>>(x, M, D, ldx, gain, bias, eps, out_f32, ld_f32,
+                                                  hi, lo, ld_bf);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_embed_stack(const float* x, const float* pos, const float* cls,
+                                 const int32_t* row_src, const int32_t* row_pos, int rows, int D,
+                                 float* out, void* stream) {
+  ASTRA_REQUIRE(D % 4 == 0, ASTRA_ERR_SHAPE, "embed: D must be a multiple of 4");
+  if (rows == 0) return ASTRA_OK;
+  embed_stack_kernel<<<grid_rows(rows, 8), 256, 0, as_stream(stream)>>>(x, pos, cls, row_src,
+                                                                       row_pos, rows, D, out);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_replica_mean(const float* reps, int N, int B, int D, float* out,
+                                  void* stream) {
+  ASTRA_REQUIRE(N >= 1, ASTRA_ERR_SHAPE, "no class-token replicas to aggregate");
+  const int bd = B * D;
+  if (bd == 0) return ASTRA_OK;
+  replica_mean_kernel<<<(bd + 255) / 256, 256, 0, as_stream(stream)>>>(reps, N, bd, out);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_gather_rows(const float* src, int lds, const int32_t* idx, int rows, int D,
+                                 float* out, int ldo, void* stream) {
+  ASTRA_REQUIRE(D % 4 == 0 && lds % 4 == 0 && ldo % 4 == 0, ASTRA_ERR_SHAPE,
+                "gather_rows: widths must be multiples of 4");
+  if (rows == 0) return ASTRA_OK;
+  gather_rows_kernel<<<grid_rows(rows, 8), 256, 0, as_stream(stream)>>>(src, lds, idx, rows, D,
+                                                                       out, ldo);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_key_map(const int32_t* key_map, int n, const int32_t* codes,
+                             int32_t* key_src, void* stream) {
+  if (n == 0) return ASTRA_OK;
+  key_map_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(key_map, n, codes, key_src);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}

@@ -1,0 +1,415 @@
+"""AstraRuntime — the B200 executor of the Astra lockstep SP forward.
+
+Reference semantics: cluster.run_inference (cluster.py:224-308) with
+_device_layer_compute (cluster.py:176-221) per device and layer.  Design:
+
+* Layout.  Every device d holds, per image b, its T_d content rows followed by its
+  class replica (if it owns one) — one flat fp32 "stack" [R, D] in HBM (the residual
+  stream).  All devices of the plan that live on this GPU are laid out back to back
+  ("virtual devices"); under torch.distributed each rank holds just its own shard.
+* Per layer: VQ encode of the content rows (tcgen05 bf16x3 + exact fp64 re-rank) ->
+  exchange of the packed codes (NCCL all-gather over NVLink; a no-op for virtual
+  devices) -> LN1 -> fused Q|K|V GEMM over local rows -> attention whose K/V tile loader
+  reads local keys from the projection buffer and remote keys straight out of the
+  per-layer codebook K/V table by code (G = 1: LN1(C)·Wk, LN1(C)·Wv are exactly the rows
+  the reference recomputes for every dequantized token) or from decoded K^/V^ (G > 1)
+  -> Wo GEMM (+residual) -> LN2 -> W1 GEMM (+bias, erf-GELU) -> W2 GEMM (+bias,
+  +residual).  Then the replica merge (device order), final LN and head GEMM.
+* Precision.  "parity": every GEMM is split bf16x3 on tcgen05 (fp32-class; indices match
+  the fp64 reference end to end), attention in fp32.  "fast": bf16 operands, fp32
+  accumulate, fp32 residual stream; VQ encode stays exact in both modes.
+* The whole forward is a fixed sequence of native launches on one stream, so it is
+  captured once into a CUDA graph (``capture``) and replayed.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native, kernels
+from .errors import ShapeError
+from .model import LN_EPS, class_owner_ids
+from .vq import DeviceCodebook, index_bits
+
+BF16 = torch.bfloat16
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _p(t: torch.Tensor | None, elem_offset: int = 0) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr() + elem_offset * t.element_size()
+
+
+class TorchDistExchange:
+    """Packed-index all-gather over torch.distributed (NCCL on NVLink/NVSwitch)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        self.dist.all_gather_into_tensor(out, inp, group=self.group)
+
+
+class AstraRuntime:
+    def __init__(self, params, plan, batch: int, mode: str = "classify",
+                 cls_mode: str = "distributed", precision: str = "parity", comm=None,
+                 device: torch.device | None = None, encode_at_one_device: bool = True,
+                 require_codebooks: bool = True):
+        if precision not in ("parity", "fast"):
+            raise ValueError("precision must be 'parity' or 'fast'")
+        if not torch.cuda.is_available():
+            raise RuntimeError("AstraRuntime needs a CUDA device (no CPU fallback)")
+        _native.load()
+        cfg = params.config
+        self.cfg, self.plan, self.B = cfg, plan, int(batch)
+        self.mode, self.cls_mode, self.precision = mode, cls_mode, precision
+        self.fast = precision == "fast"
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.comm = comm
+        self.D, self.H, self.L = cfg.hidden, cfg.heads, cfg.layers
+        self.dk = cfg.hidden // cfg.heads
+        if self.dk not in (8, 16, 32, 64, 128):
+            raise ShapeError(f"head_dim {self.dk} unsupported")
+        self.T, self.N = plan.tokens, plan.devices
+        self.G, self.K = cfg.groups, cfg.codebook_size
+        self.bits = index_bits(self.K)
+        self.encode_at_one_device = encode_at_one_device
+        self.require_codebooks = require_codebooks or plan.devices > 1
+        self.capture_inputs = None   # setup hook: per-layer block inputs (codebook fitting)
+        if comm is not None and comm.world != self.N:
+            raise ShapeError("world size must equal plan.devices")
+        self.local = list(range(self.N)) if comm is None else [comm.rank]
+        self.owners = [] if cfg.causal else (class_owner_ids(plan, cls_mode)
+                                             if plan.class_replication else [])
+        self._build_layout()
+        self._upload(params)
+        self._alloc()
+        self.graph = None
+        self.trace = None   # test hook: list collecting idx_all per layer
+
+    # ------------------------------------------------------------------ layout
+    def _build_layout(self):
+        T, B = self.T, self.B
+        sizes = self.plan.shard_sizes()
+        starts = [r[0] for r in self.plan.ranges]
+        owner = self.plan.owner_of()
+        gofs = np.concatenate([[0], np.cumsum([B * s for s in sizes])]).astype(np.int64)
+        rows = 0
+        content, row_src, row_pos, segs, key_map, key_pos, rep_rows = [], [], [], [], [], [], []
+        self.row_base = {}
+        for v in self.local:
+            rep = 1 if v in self.owners else 0
+            for b in range(B):
+                base = rows
+                self.row_base[(v, b)] = base
+                for r in range(sizes[v]):
+                    content.append(base + r)
+                    row_src.append(b * T + starts[v] + r)
+                    row_pos.append(starts[v] + r)
+                if rep:
+                    row_src.append(-1)
+                    row_pos.append(0)
+                    rep_rows.append(base + sizes[v])
+                k0 = len(key_map)
+                for j in range(T):
+                    e = int(owner[j])
+                    if e == v:
+                        key_map.append(base + j - starts[v])
+                    else:
+                        key_map.append(-int(gofs[e] + b * sizes[e] + (j - starts[e]) + 1))
+                    key_pos.append(j)
+                if rep:
+                    key_map.append(base + sizes[v])
+                    key_pos.append(-1)
+                segs.append([base, sizes[v] + rep, starts[v], sizes[v], k0, T + rep])
+                rows += sizes[v] + rep
+        dev = self.device
+        i32 = lambda a: torch.tensor(np.asarray(a, dtype=np.int32), device=dev)  # noqa: E731
+        self.R = rows
+        self.sizes, self.starts = sizes, starts
+        self.n_content = len(content)
+        self.n_content_all = int(gofs[-1])
+        self.gofs = gofs
+        self.content_rows = i32(content)
+        self.row_src, self.row_pos = i32(row_src), i32(row_pos)
+        self.segs = i32(np.asarray(segs).reshape(-1))
+        self.n_segs = len(segs)
+        self.key_map, self.key_pos = i32(key_map), i32(key_pos)
+        self.n_keys = len(key_map)
+        self.rep_rows = i32(rep_rows) if rep_rows else None
+        self.max_nq = max(s[1] for s in segs)
+        self.has_remote = self.N > 1
+        self.payload_bits = [B * s * self.G * self.bits for s in sizes]
+
+    # ------------------------------------------------------------------ params
+    def _wt(self, w_in_out: np.ndarray):
+        """Reference weight [D_in, D_out] -> B operand [D_out, D_in] (hi[, lo])."""
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(w_in_out, np.float32).T)).to(self.device)
+        if self.fast:
+            return t.to(BF16).contiguous(), None
+        hi, lo = kernels.split_bf16(t)
+        return hi.contiguous(), lo.contiguous()
+
+    def _upload(self, params):
+        dev = self.device
+        f32 = lambda a: torch.from_numpy(np.ascontiguousarray(np.asarray(a.data if hasattr(a, "data") else a, np.float32))).to(dev)  # noqa: E501,E731
+        self.layers = []
+        for i, bp in enumerate(params.blocks):
+            wqkv = np.concatenate([bp.wq.data, bp.wk.data, bp.wv.data], axis=1)
+            lay = dict(
+                wqkv=self._wt(wqkv), wo=self._wt(bp.wo.data), w1=self._wt(bp.w1.data),
+                w2=self._wt(bp.w2.data), b1=f32(bp.b1), b2=f32(bp.b2),
+                ln1_g=f32(bp.ln1_gain), ln1_b=f32(bp.ln1_bias),
+                ln2_g=f32(bp.ln2_gain), ln2_b=f32(bp.ln2_bias))
+            if bp.codebook is None:
+                if self.require_codebooks:
+                    raise ValueError(f"layer {i} has no codebook")
+                lay["cb"] = None
+            else:
+                tables = np.stack([np.asarray(c, np.float32) for c in bp.codebook.centroids])
+                lay["cb"] = DeviceCodebook(torch.from_numpy(tables).to(dev), layer_id=i)
+            self.layers.append(lay)
+        self.pos = f32(params.pos)
+        self.cls = f32(params.cls).reshape(-1) if params.cls is not None else None
+        self.emb = f32(params.embedding) if params.embedding is not None else None
+        self.final_g, self.final_b = f32(params.final_gain), f32(params.final_bias)
+        self.head = self._wt(params.head.data)
+        self.classes = params.head.data.shape[1]
+        if self.has_remote and self.G == 1:
+            self._build_kv_tables()
+
+    def _kv_rows(self, lay, x_f32: torch.Tensor, out: torch.Tensor, ln_hi, ln_lo):
+        """K|V projection of fp32 rows: LN1 -> [Wk;Wv] GEMM (same kernels as the local path)."""
+        m = x_f32.shape[0]
+        D = self.D
+        _native.call("astra_layernorm", x_f32.data_ptr(), m, D, x_f32.stride(0),
+                     lay["ln1_g"].data_ptr(), lay["ln1_b"].data_ptr(), LN_EPS, None, 0,
+                     ln_hi.data_ptr(), _p(ln_lo), D, _stream())
+        whi, wlo = lay["wqkv"]
+        kernels.gemm(ln_hi[:m], whi[D:], a_lo=None if ln_lo is None else ln_lo[:m],
+                     b_lo=None if wlo is None else wlo[D:],
+                     out_f32=None if self.fast else out, out_hi=out if self.fast else None)
+
+    def _build_kv_tables(self):
+        """G = 1: per-layer codebook K/V tables [K, 2D] = (LN1(C) Wk | LN1(C) Wv)."""
+        D, K = self.D, self.K
+        ln_hi = torch.empty(K, D, dtype=BF16, device=self.device)
+        ln_lo = None if self.fast else torch.empty_like(ln_hi)
+        for lay in self.layers:
+            c = lay["cb"].centroids[0]
+            tab = torch.empty(K, 2 * D, dtype=BF16 if self.fast else torch.float32,
+                              device=self.device)
+            self._kv_rows(lay, c, tab, ln_hi, ln_lo)
+            lay["kvtab"] = tab
+        torch.cuda.current_stream().synchronize()
+
+    # ----------------------------------------------------------------- buffers
+    def _alloc(self):
+        dev, R, D, B = self.device, self.R, self.D, self.B
+        e = lambda *s, dt=torch.float32: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
+        self.x_in = e(B * self.T, D)
+        self.X, self.Hres = e(R, D), e(R, D)
+        self.ln_hi = e(R, D, dt=BF16)
+        self.ln_lo = None if self.fast else e(R, D, dt=BF16)
+        self.qkv = e(R, 3 * D, dt=BF16 if self.fast else torch.float32)
+        self.o_hi = e(R, D, dt=BF16)
+        self.o_lo = None if self.fast else e(R, D, dt=BF16)
+        self.f_hi = e(R, 4 * D, dt=BF16)
+        self.f_lo = None if self.fast else e(R, 4 * D, dt=BF16)
+        self.idx_local = e(max(self.n_content, 1), self.G, dt=torch.int32)
+        self.idx_all = self.idx_local if self.comm is None else e(self.n_content_all, self.G,
+                                                                  dt=torch.int32)
+        self.key_src = e(self.n_keys, dt=torch.int32)
+        self.key_src.copy_(self.key_map)
+        cb0 = self.layers[0]["cb"]
+        self.vq_ws = e(max(cb0.workspace_bytes(max(self.n_content, 1)) if cb0 else 1, 1),
+                       dt=torch.uint8)
+        self.vq_stats = torch.zeros(4, dtype=torch.int32, device=dev)
+        if self.comm is not None:
+            wmax = (B * max(self.sizes) * self.G * self.bits + 31) // 32
+            self.wmax = max(wmax, 1)
+            self.words_local = torch.zeros(self.wmax, dtype=torch.int32, device=dev)
+            self.words_all = torch.zeros(self.N * self.wmax, dtype=torch.int32, device=dev)
+            self.unpack_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        if self.has_remote and self.G > 1:
+            n = self.n_content_all
+            self.xhat = e(n, D)
+            self.hat_hi = e(n, D, dt=BF16)
+            self.hat_lo = None if self.fast else e(n, D, dt=BF16)
+            self.kvhat = e(n, 2 * D, dt=BF16 if self.fast else torch.float32)
+            self.dec_err = torch.zeros(1, dtype=torch.int32, device=dev)
+        n_rep_local = 0 if self.rep_rows is None else self.rep_rows.numel()
+        if self.mode == "classify":
+            self.reps_local = e(max(n_rep_local, 1), D)
+            self.reps_all = e(len(self.owners) * B, D) if self.comm is not None else self.reps_local
+            self.pooled = e(B, D)
+            self.pool_hi = e(B, D, dt=BF16)
+            self.pool_lo = None if self.fast else e(B, D, dt=BF16)
+            self.logits = e(B, self.classes)
+
+    # ----------------------------------------------------------------- forward
+    def _exchange(self, layer: int):
+        """Make every device's layer-`layer` codes visible to this GPU (cluster.py:276-279)."""
+        if self.comm is None:
+            return
+        kernels.pack_indices(self.idx_local, self.bits, out=self.words_local)
+        self.comm.all_gather(self.words_all, self.words_local)
+        for e in range(self.N):
+            cnt = self.B * self.sizes[e] * self.G
+            kernels.unpack_indices(self.words_all[e * self.wmax:], cnt, self.bits, self.K,
+                                   out=self.idx_all.view(-1)[int(self.gofs[e]) * self.G:],
+                                   err=self.unpack_err)
+
+    def _layer(self, l: int):
+        lay = self.layers[l]
+        D, R, s = self.D, self.R, _stream()
+        cb = lay["cb"]
+        if self.capture_inputs is not None:
+            self.capture_inputs.append(self.X[self.content_rows.long()].clone())
+        # 1. VQ encode of this GPU's content tokens (cluster.py:272-275)
+        if cb is not None and (self.has_remote or self.encode_at_one_device):
+            cb.encode(self.X, out=self.idx_local, rows=self.content_rows, workspace=self.vq_ws,
+                      stats=self.vq_stats)
+        # 2. exchange + remote K/V view
+        if self.has_remote:
+            self._exchange(l)
+            if self.G == 1:
+                _native.call("astra_key_map", self.key_map.data_ptr(), self.n_keys,
+                             self.idx_all.data_ptr(), self.key_src.data_ptr(), s)
+                remote = lay["kvtab"]
+            else:
+                cb.decode(self.idx_all, out=self.xhat, err=self.dec_err)
+                self._kv_rows(lay, self.xhat, self.kvhat, self.hat_hi, self.hat_lo)
+                remote = self.kvhat
+        else:
+            remote = self.qkv
+        if self.trace is not None:
+            self.trace.append(self.idx_all.clone())
+        # 3. LN1 over the local stack (content + replica)
+        _native.call("astra_layernorm", self.X.data_ptr(), R, D, D, lay["ln1_g"].data_ptr(),
+                     lay["ln1_b"].data_ptr(), LN_EPS, None, 0, self.ln_hi.data_ptr(),
+                     _p(self.ln_lo), D, s)
+        # 4. fused Q|K|V projection
+        whi, wlo = lay["wqkv"]
+        kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo,
+                     out_f32=None if self.fast else self.qkv, out_hi=self.qkv if self.fast else None)
+        # 5. mixed-precision attention
+        ld_r = remote.stride(0)
+        _native.call("astra_attention", self.qkv.data_ptr(), 3 * D, _p(self.qkv, D),
+                     _p(self.qkv, 2 * D), 3 * D, _p(remote, 0 if remote is self.qkv else 0),
+                     _p(remote, D), ld_r, self.key_src.data_ptr(), self.key_pos.data_ptr(),
+                     self.segs.data_ptr(), self.n_segs, self.max_nq, self.H, self.dk,
+                     int(self.cfg.causal), int(self.fast), float(np.float32(1.0 / math.sqrt(self.dk))),
+                     None, self.o_hi.data_ptr(), _p(self.o_lo), D, s)
+        # 6. h = stack + attn Wo
+        whi, wlo = lay["wo"]
+        kernels.gemm(self.o_hi, whi, a_lo=self.o_lo, b_lo=wlo, residual=self.X, out_f32=self.Hres)
+        # 7. LN2 -> W1 (+b1, GELU) -> W2 (+b2, +h)
+        _native.call("astra_layernorm", self.Hres.data_ptr(), R, D, D, lay["ln2_g"].data_ptr(),
+                     lay["ln2_b"].data_ptr(), LN_EPS, None, 0, self.ln_hi.data_ptr(),
+                     _p(self.ln_lo), D, s)
+        whi, wlo = lay["w1"]
+        kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo, bias=lay["b1"], gelu=True,
+                     out_hi=self.f_hi, out_lo=self.f_lo)
+        whi, wlo = lay["w2"]
+        kernels.gemm(self.f_hi, whi, a_lo=self.f_lo, b_lo=wlo, bias=lay["b2"],
+                     residual=self.Hres, out_f32=self.X)
+
+    def _embed(self):
+        _native.call("astra_embed_stack", self.x_in.data_ptr(), self.pos.data_ptr(),
+                     _p(self.cls), self.row_src.data_ptr(), self.row_pos.data_ptr(), self.R,
+                     self.D, self.X.data_ptr(), _stream())
+
+    def _classify_tail(self):
+        D, B, s = self.D, self.B, _stream()
+        n_loc = self.rep_rows.numel() if self.rep_rows is not None else 0
+        if n_loc:
+            _native.call("astra_gather_rows", self.X.data_ptr(), D, self.rep_rows.data_ptr(),
+                         n_loc, D, self.reps_local.data_ptr(), D, s)
+        if self.comm is not None:
+            self._gather_replicas()
+        _native.call("astra_replica_mean", self.reps_all.data_ptr(), len(self.owners), B, D,
+                     self.pooled.data_ptr(), s)
+        _native.call("astra_layernorm", self.pooled.data_ptr(), B, D, D, self.final_g.data_ptr(),
+                     self.final_b.data_ptr(), LN_EPS, None, 0, self.pool_hi.data_ptr(),
+                     _p(self.pool_lo), D, s)
+        whi, wlo = self.head
+        kernels.gemm(self.pool_hi, whi, a_lo=self.pool_lo, b_lo=wlo, out_f32=self.logits)
+
+    def _gather_replicas(self):
+        """Replica merge across ranks (cluster.py:290-292): all-gather [B, D] per owner."""
+        B, D = self.B, self.D
+        buf = getattr(self, "_rep_gather", None)
+        if buf is None:
+            self._rep_gather = buf = torch.zeros(self.N * B, D, device=self.device)
+            self._rep_send = torch.zeros(B, D, device=self.device)
+        if self.rep_rows is not None:
+            self._rep_send.copy_(self.reps_local[:B])
+        else:
+            self._rep_send.zero_()
+        self.comm.all_gather(buf, self._rep_send)
+        for i, e in enumerate(self.owners):
+            self.reps_all[i * B:(i + 1) * B].copy_(buf[e * B:(e + 1) * B])
+
+    def forward(self):
+        """Run the forward on the already-staged input ``self.x_in``; logits in ``self.logits``."""
+        self._embed()
+        for l in range(self.L):
+            self._layer(l)
+        if self.mode == "classify":
+            self._classify_tail()
+        return self.logits
+
+    # -------------------------------------------------------------- CUDA graph
+    def capture(self, warmup: int = 1):
+        """Record ``forward`` (fixed buffers, fixed launch sequence) into a CUDA graph."""
+        for _ in range(warmup):
+            self.forward()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.forward()
+        self.graph = g
+        return g
+
+    def run(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.forward()
+        return self.logits
+
+    # ------------------------------------------------------------------ host API
+    def stage_input(self, xs):
+        """Copy inputs [B, T, D] (host NumPy/pinned tensor or device tensor) into HBM."""
+        if isinstance(xs, np.ndarray):
+            xs = torch.from_numpy(np.ascontiguousarray(xs, dtype=np.float32))
+        if xs.shape != (self.B, self.T, self.D):
+            raise ShapeError(f"expected inputs [{self.B}, {self.T}, {self.D}], got {tuple(xs.shape)}")
+        self.x_in.view(self.B, self.T, self.D).copy_(xs, non_blocking=True)
+
+    def record_ledger(self, ledger):
+        if ledger is None or self.N <= 1:
+            return
+        for l in range(self.L):
+            ledger.record_exchange(l, self.payload_bits)
+
+    def classify_numpy(self, xs: np.ndarray, ledger=None) -> np.ndarray:
+        self.stage_input(xs)
+        out = self.run().cpu().numpy().copy()
+        self.record_ledger(ledger)
+        return out
+
+    def indices_after_layer(self):
+        return self.idx_all

@@ -219,3 +219,40 @@ def dequantize(codebook: Codebook, q: QuantizedTokens):
     out = dc.decode(torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int32)).to(
         dc.centroids.device))
     return out.cpu().numpy()
+
+
+MAGIC = b"AVQ1"
+
+
+def save_codebook(codebook: Codebook) -> bytes:
+    """AVQ1 blob (vq.py:328-339): magic, (layer, G, K, D/G) LE u32, fp32 centroids
+    group-major, then fp64 EMA counts and sums."""
+    import struct
+    g, k, gd = codebook.groups, codebook.size, codebook.group_dim
+    counts = codebook.ema_counts if codebook.ema_counts is not None else np.zeros((g, k))
+    sums = codebook.ema_sums if codebook.ema_sums is not None else [np.zeros((k, gd))] * g
+    head = MAGIC + struct.pack("<4I", codebook.layer_id, g, k, gd)
+    body = b"".join(np.ascontiguousarray(c, dtype="<f4").tobytes() for c in codebook.centroids)
+    ema = np.ascontiguousarray(counts, dtype="<f8").tobytes()
+    ema += b"".join(np.ascontiguousarray(s, dtype="<f8").tobytes() for s in sums)
+    return head + body + ema
+
+
+def load_codebook(blob: bytes) -> Codebook:
+    """Inverse of save_codebook (vq.py:342-361), same validation."""
+    import struct
+    if len(blob) < 20 or blob[:4] != MAGIC:
+        raise ValueError("not a codebook blob (bad magic)")
+    layer_id, groups, k, gd = struct.unpack("<4I", blob[4:20])
+    expect = 20 + 4 * groups * k * gd + 8 * groups * k + 8 * groups * k * gd
+    if len(blob) != expect:
+        raise ValueError(f"codebook blob length {len(blob)} != expected {expect}")
+    flat = np.frombuffer(blob, dtype="<f4", offset=20, count=groups * k * gd)
+    tables = [flat[g * k * gd:(g + 1) * k * gd].reshape(k, gd).copy() for g in range(groups)]
+    off = 20 + 4 * groups * k * gd
+    counts = np.frombuffer(blob, dtype="<f8", offset=off, count=groups * k).reshape(groups, k).copy()
+    off += 8 * groups * k
+    sums_flat = np.frombuffer(blob, dtype="<f8", offset=off)
+    sums = [sums_flat[g * k * gd:(g + 1) * k * gd].reshape(k, gd).copy() for g in range(groups)]
+    return Codebook(layer_id=layer_id, groups=groups, centroids=tables, ema_counts=counts,
+                    ema_sums=sums)
