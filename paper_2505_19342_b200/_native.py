@@ -90,6 +90,21 @@ def check(status: int, what: str = "") -> None:
     raise RuntimeError(text)
 
 
+# kernels each C-ABI call enqueues (for launch accounting in bench.py)
+LAUNCHES = {"astra_vq_encode": 3, "astra_vq_prepare": 2}
+_counter: dict | None = None
+
+
+def count_launches(enable: bool) -> dict | None:
+    """Start (enable=True) or stop counting native kernel launches; returns the tally."""
+    global _counter
+    out = _counter
+    _counter = {} if enable else None
+    return out
+
+
 def call(name: str, *args) -> None:
     lib = load()
     check(getattr(lib, name)(*args), name)
+    if _counter is not None:
+        _counter[name] = _counter.get(name, 0) + LAUNCHES.get(name, 1)

@@ -24,6 +24,7 @@ _device_layer_compute (cluster.py:176-221) per device and layer.  Design:
 
 from __future__ import annotations
 
+import contextlib
 import math
 
 import numpy as np
@@ -97,6 +98,7 @@ class AstraRuntime:
         self._alloc()
         self.graph = None
         self.trace = None   # test hook: list collecting idx_all per layer
+        self.profile = None  # bench hook: {op name: [(start_event, end_event), ...]}
 
     # ------------------------------------------------------------------ layout
     def _build_layout(self):
@@ -259,6 +261,19 @@ class AstraRuntime:
             self.logits = e(B, self.classes)
 
     # ----------------------------------------------------------------- forward
+    def _op(self, name: str):
+        if self.profile is None:
+            return contextlib.nullcontext()
+        return self._timed(name)
+
+    @contextlib.contextmanager
+    def _timed(self, name: str):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        yield
+        e.record()
+        self.profile.setdefault(name, []).append((s, e))
+
     def _exchange(self, layer: int):
         """Make every device's layer-`layer` codes visible to this GPU (cluster.py:276-279)."""
         if self.comm is None:
@@ -279,11 +294,13 @@ class AstraRuntime:
             self.capture_inputs.append(self.X[self.content_rows.long()].clone())
         # 1. VQ encode of this GPU's content tokens (cluster.py:272-275)
         if cb is not None and (self.has_remote or self.encode_at_one_device):
-            cb.encode(self.X, out=self.idx_local, rows=self.content_rows, workspace=self.vq_ws,
-                      stats=self.vq_stats)
+            with self._op("vq_encode"):
+                cb.encode(self.X, out=self.idx_local, rows=self.content_rows,
+                          workspace=self.vq_ws, stats=self.vq_stats)
         # 2. exchange + remote K/V view
         if self.has_remote:
-            self._exchange(l)
+            with self._op("exchange"):
+                self._exchange(l)
             if self.G == 1:
                 _native.call("astra_key_map", self.key_map.data_ptr(), self.n_keys,
                              self.idx_all.data_ptr(), self.key_src.data_ptr(), s)
@@ -297,16 +314,20 @@ class AstraRuntime:
         if self.trace is not None:
             self.trace.append(self.idx_all.clone())
         # 3. LN1 over the local stack (content + replica)
-        _native.call("astra_layernorm", self.X.data_ptr(), R, D, D, lay["ln1_g"].data_ptr(),
+        with self._op("ln1"):
+            _native.call("astra_layernorm", self.X.data_ptr(), R, D, D, lay["ln1_g"].data_ptr(),
                      lay["ln1_b"].data_ptr(), LN_EPS, None, 0, self.ln_hi.data_ptr(),
                      _p(self.ln_lo), D, s)
         # 4. fused Q|K|V projection
         whi, wlo = lay["wqkv"]
-        kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo,
-                     out_f32=None if self.fast else self.qkv, out_hi=self.qkv if self.fast else None)
+        with self._op("gemm_qkv"):
+            kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo,
+                         out_f32=None if self.fast else self.qkv,
+                         out_hi=self.qkv if self.fast else None)
         # 5. mixed-precision attention
         ld_r = remote.stride(0)
-        _native.call("astra_attention", self.qkv.data_ptr(), 3 * D, _p(self.qkv, D),
+        with self._op("attention"):
+            _native.call("astra_attention", self.qkv.data_ptr(), 3 * D, _p(self.qkv, D),
                      _p(self.qkv, 2 * D), 3 * D, _p(remote, 0 if remote is self.qkv else 0),
                      _p(remote, D), ld_r, self.key_src.data_ptr(), self.key_pos.data_ptr(),
                      self.segs.data_ptr(), self.n_segs, self.max_nq, self.H, self.dk,
@@ -314,17 +335,22 @@ class AstraRuntime:
                      None, self.o_hi.data_ptr(), _p(self.o_lo), D, s)
         # 6. h = stack + attn Wo
         whi, wlo = lay["wo"]
-        kernels.gemm(self.o_hi, whi, a_lo=self.o_lo, b_lo=wlo, residual=self.X, out_f32=self.Hres)
+        with self._op("gemm_wo"):
+            kernels.gemm(self.o_hi, whi, a_lo=self.o_lo, b_lo=wlo, residual=self.X,
+                         out_f32=self.Hres)
         # 7. LN2 -> W1 (+b1, GELU) -> W2 (+b2, +h)
-        _native.call("astra_layernorm", self.Hres.data_ptr(), R, D, D, lay["ln2_g"].data_ptr(),
+        with self._op("ln2"):
+            _native.call("astra_layernorm", self.Hres.data_ptr(), R, D, D, lay["ln2_g"].data_ptr(),
                      lay["ln2_b"].data_ptr(), LN_EPS, None, 0, self.ln_hi.data_ptr(),
                      _p(self.ln_lo), D, s)
         whi, wlo = lay["w1"]
-        kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo, bias=lay["b1"], gelu=True,
-                     out_hi=self.f_hi, out_lo=self.f_lo)
+        with self._op("gemm_w1"):
+            kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo, bias=lay["b1"], gelu=True,
+                         out_hi=self.f_hi, out_lo=self.f_lo)
         whi, wlo = lay["w2"]
-        kernels.gemm(self.f_hi, whi, a_lo=self.f_lo, b_lo=wlo, bias=lay["b2"],
-                     residual=self.Hres, out_f32=self.X)
+        with self._op("gemm_w2"):
+            kernels.gemm(self.f_hi, whi, a_lo=self.f_lo, b_lo=wlo, bias=lay["b2"],
+                         residual=self.Hres, out_f32=self.X)
 
     def _embed(self):
         _native.call("astra_embed_stack", self.x_in.data_ptr(), self.pos.data_ptr(),
@@ -364,11 +390,13 @@ class AstraRuntime:
 
     def forward(self):
         """Run the forward on the already-staged input ``self.x_in``; logits in ``self.logits``."""
-        self._embed()
+        with self._op("embed"):
+            self._embed()
         for l in range(self.L):
             self._layer(l)
         if self.mode == "classify":
-            self._classify_tail()
+            with self._op("tail"):
+                self._classify_tail()
         return self.logits
 
     # -------------------------------------------------------------- CUDA graph
