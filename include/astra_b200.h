@@ -153,6 +153,17 @@ int astra_attention(const void* q, int ldq, const void* k_local, const void* v_l
                     float scale, float* out_f32, void* out_hi, void* out_lo, int ld_out,
                     void* stream);
 
+/* Dense-mask form for the operator API (attention.multihead_attention,
+ * attention.py:50-73): q [R, D], k/v [C, D] fp32, mask uint8 [R, C] (nonzero =
+ * visible; every row must see a key), scratch >= 6 + 2*C int32 (device). */
+int astra_attention_masked(const float* q, const float* k, const float* v, int R, int C, int D,
+                           int heads, const uint8_t* mask, int32_t* scratch, float* out,
+                           void* stream);
+
+/* Route astra_attention to the fp32 SIMT kernel even when the tcgen05 bf16
+ * kernel applies (test / A-B hook). */
+int astra_attention_force_simt(int enable);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,6 +42,9 @@ SIGNATURES: dict[str, list] = {
     "astra_attention": [_vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int,
                         _c_int, _c_int, _c_int, _c_int, _c_int, ctypes.c_float, _vp, _vp, _vp,
                         _c_int, _vp],
+    "astra_attention_force_simt": [_c_int],
+    "astra_attention_masked": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
+                               _vp],
 }
 _RESTYPES = {"astra_last_error": ctypes.c_char_p, "astra_vq_encode_workspace": ctypes.c_longlong}
 

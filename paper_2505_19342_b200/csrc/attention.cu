@@ -15,6 +15,8 @@
 // v1 is an fp32 SIMT flash-style kernel (online softmax over 64-key tiles, 64x64 fp32 K/V tiles
 // in padded shared memory).  It is exact enough for the fp32 parity mode and general in T.
 #include <climits>
+#include <cmath>
+#include <vector>
 
 #include "host_common.h"
 #include "ptx.cuh"
@@ -39,6 +41,8 @@ struct AttnArgs {
   __nv_bfloat16* out_hi;
   __nv_bfloat16* out_lo;
   int ld_out;
+  const uint8_t* mask;  // optional dense mask [rows, mask_ld] indexed by (q0 + qi, key)
+  int mask_ld;
 };
 
 constexpr int kAQ = 64;    // queries per CTA
@@ -118,7 +122,8 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
     for (int i = 0; i < 16; ++i) {
       const int kj = part + 4 * i;
       const int kp = sKpos[kj];
-      const bool vis = (kt + kj < nk) && (!a.causal || kp <= qpos) && kp != INT_MAX;
+      bool vis = (kt + kj < nk) && (!a.causal || kp <= qpos) && kp != INT_MAX;
+      if (a.mask && vis) vis = a.mask[(size_t)(q0 + (qvalid ? qi : 0)) * a.mask_ld + kt + kj] != 0;
       float dot = 0.f;
 #pragma unroll
       for (int d = 0; d < kDH; ++d) dot = fmaf(q[d], sK[kj * kPad + d], dot);
@@ -167,6 +172,223 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
   }
 }
 
+// ----------------------------------------------------------------------------------------
+// tcgen05 flash attention (bf16 fast path, head_dim 64).  One CTA (4 warps) per
+// (segment, head, 128-query tile); keys stream in chunks of 128:
+//   S = Q K^T on the tensor core (M=128, N=128, K=64) into TMEM,
+//   softmax in registers (thread = query row, tcgen05.ld of its TMEM lane),
+//   P (bf16) written to shared memory in the UMMA K-major SW128 layout,
+//   O_chunk = P V on the tensor core (M=128, N=64, K=128; V used MN-major as stored),
+//   online-softmax rescale of the running output in registers.
+// K/V rows are gathered with cp.async through key_src, which fuses the VQ decode
+// (codebook K/V table rows) into the tile load.
+constexpr int kTQ = 128, kTK = 128;
+static bool g_force_simt_attention = false;  // test hook (astra_attention_force_simt)
+constexpr int kTcSmem = 16384 * 3 + 32768 + 512 + 64 + 1024;
+
+__host__ __device__ constexpr uint32_t idesc_bf16_f32_bmn(uint32_t M, uint32_t N) {
+  return idesc_bf16_f32(M, N) | (1u << 16);  // B operand MN-major
+}
+
+__global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* sQ = sm;
+  uint8_t* sK = sm + 16384;
+  uint8_t* sV = sm + 32768;
+  uint8_t* sP = sm + 49152;
+  int* sKpos = reinterpret_cast<int*>(sm + 81920);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 81920 + 512);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int seg = blockIdx.x, h = blockIdx.y, qt = blockIdx.z;
+  const int* sg = a.segs + seg * 6;
+  const int q0 = sg[0], nq = sg[1], qpos0 = sg[2], ncontent = sg[3], k0 = sg[4], nk = sg[5];
+  if (qt * kTQ >= nq) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int hoff = h * 64;
+  const __nv_bfloat16* Q = reinterpret_cast<const __nv_bfloat16*>(a.q);
+  const __nv_bfloat16* KL = reinterpret_cast<const __nv_bfloat16*>(a.k_local);
+  const __nv_bfloat16* VL = reinterpret_cast<const __nv_bfloat16*>(a.v_local);
+  const __nv_bfloat16* KR = reinterpret_cast<const __nv_bfloat16*>(a.k_remote);
+  const __nv_bfloat16* VR = reinterpret_cast<const __nv_bfloat16*>(a.v_remote);
+
+  if (warp == 0) tmem_alloc<256>(tslot);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  const uint32_t q_s = smem_u32(sQ), k_s = smem_u32(sK), v_s = smem_u32(sV), p_s = smem_u32(sP);
+  for (int i = tid; i < kTQ * 8; i += 128) {
+    const int r = i >> 3, c = i & 7, qi = qt * kTQ + r;
+    const uint32_t dst = q_s + sw128_offset(r, c);
+    if (qi < nq)
+      cp_async16(dst, Q + (size_t)(q0 + qi) * a.ldq + hoff + c * 8);
+    else
+      *reinterpret_cast<uint4*>(sQ + sw128_offset(r, c)) = make_uint4(0, 0, 0, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t tS = tmem, tO = tmem + 128;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+
+  const int r = warp * 32 + lane;
+  const int qi = qt * kTQ + r;
+  const int qpos = qi < ncontent ? qpos0 + qi : INT_MAX;
+  const float sl2 = a.scale * 1.4426950408889634f;  // exp(x) = exp2(x * log2 e)
+  float m = -INFINITY, l = 0.f;
+  float o[64];
+#pragma unroll
+  for (int d = 0; d < 64; ++d) o[d] = 0.f;
+  uint32_t phase = 0;
+
+  for (int kc = 0; kc < nk; kc += kTK) {
+    for (int i = tid; i < kTK * 8; i += 128) {
+      const int j = i >> 3, c = i & 7, key = kc + j;
+      const uint32_t off = sw128_offset(j, c);
+      if (key < nk) {
+        const int src = a.key_src[k0 + key];
+        const __nv_bfloat16 *kp, *vp;
+        if (src >= 0) {
+          kp = KL + (size_t)src * a.ld_local;
+          vp = VL + (size_t)src * a.ld_local;
+        } else {
+          kp = KR + (size_t)(-(src + 1)) * a.ld_remote;
+          vp = VR + (size_t)(-(src + 1)) * a.ld_remote;
+        }
+        cp_async16(k_s + off, kp + hoff + c * 8);
+        cp_async16(v_s + off, vp + hoff + c * 8);
+      } else {
+        *reinterpret_cast<uint4*>(sK + off) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(sV + off) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    sKpos[tid] = (kc + tid < nk) ? a.key_pos[k0 + kc + tid] : INT_MAX;
+    cp_async_wait_all();
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_f16(tS, sdesc_kmajor_sw128(q_s + kk * 32), sdesc_kmajor_sw128(k_s + kk * 32),
+                 idesc_bf16_f32(128, 128), kk > 0 ? 1u : 0u);
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+
+    // ---- softmax (row r): pass 1 max, pass 2 exp + P store
+    float cmax = -INFINITY;
+#pragma unroll 1
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t rr[32];
+      tmem_ld32(tS + lane_off + cc * 32, rr);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int kp = sKpos[cc * 32 + j];
+        const bool vis = kp != INT_MAX && (!a.causal || kp <= qpos);
+        if (vis) cmax = fmaxf(cmax, __uint_as_float(rr[j]));
+      }
+    }
+    const float mnew = fmaxf(m, cmax * sl2);
+    const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mnew);
+    float lsum = 0.f;
+#pragma unroll 1
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t rr[32];
+      tmem_ld32(tS + lane_off + cc * 32, rr);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        float p2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int kp = sKpos[cc * 32 + j + u];
+          const bool vis = kp != INT_MAX && (!a.causal || kp <= qpos);
+          p2[u] = vis ? exp2f(__uint_as_float(rr[j + u]) * sl2 - mnew) : 0.f;
+        }
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
+        // sum what the tensor core will multiply (the bf16-rounded probabilities)
+        lsum += __low2float(b2) + __high2float(b2);
+        pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      const int col0 = cc * 32;                 // key within chunk
+      uint8_t* blk = sP + (col0 >> 6) * 16384;  // 64-key K-block
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int chunk = ((col0 & 63) >> 3) + q;
+        *reinterpret_cast<uint4*>(blk + sw128_offset(r, chunk)) =
+            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
+    }
+    l = l * corr + lsum;
+    m = mnew;
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        umma_f16(tO, sdesc_kmajor_sw128(p_s + (kk >> 2) * 16384 + (kk & 3) * 32),
+                 sdesc_mnmajor_sw128(v_s + kk * 2048, 8192), idesc_bf16_f32_bmn(128, 64),
+                 kk > 0 ? 1u : 0u);
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      uint32_t r0[32], r1[32];
+      tmem_ld32(tO + lane_off, r0);
+      tmem_ld32(tO + lane_off + 32, r1);
+      tmem_ld_wait();
+#pragma unroll
+      for (int d = 0; d < 32; ++d) {
+        o[d] = fmaf(o[d], corr, __uint_as_float(r0[d]));
+        o[32 + d] = fmaf(o[32 + d], corr, __uint_as_float(r1[d]));
+      }
+    }
+    tc_fence_before();
+    __syncthreads();
+  }
+
+  if (qi < nq) {
+    const float inv = 1.0f / l;
+    const size_t ob = (size_t)(q0 + qi) * a.ld_out + hoff;
+    if (a.out_hi) {
+#pragma unroll
+      for (int d = 0; d < 64; d += 8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(o[d + 2 * u] * inv, o[d + 2 * u + 1] * inv);
+          w[u] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(a.out_hi + ob + d) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    if (a.out_f32) {
+#pragma unroll
+      for (int d = 0; d < 64; ++d) a.out_f32[ob + d] = o[d] * inv;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
 template <int DH>
 static int launch_attn(const AttnArgs& a, dim3 grid, cudaStream_t st) {
   constexpr int smem = 2 * kAK * (DH + 1) * 4 + kAQ * (kAK + 1) * 4 + kAK * 4;
@@ -196,7 +418,7 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
                                const int32_t* segs, int num_segs, int max_nq, int heads,
                                int head_dim, int causal, int in_bf16, float scale, float* out_f32,
                                void* out_hi, void* out_lo, int ld_out, void* stream) {
-  ASTRA_REQUIRE(head_dim == 8 || head_dim == 16 || head_dim == 32 || head_dim == 64 ||
+  ASTRA_REQUIRE(head_dim == 4 || head_dim == 8 || head_dim == 16 || head_dim == 32 || head_dim == 64 ||
                     head_dim == 128,
                 ASTRA_ERR_SHAPE, "attention: head_dim %d unsupported", head_dim);
   ASTRA_REQUIRE(heads >= 1 && num_segs >= 0 && max_nq >= 0, ASTRA_ERR_SHAPE, "attention: bad shape");
@@ -205,10 +427,28 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
              key_src, key_pos, segs,    num_segs, heads,   head_dim, causal,   in_bf16,
              scale,   out_f32, reinterpret_cast<__nv_bfloat16*>(out_hi),
              reinterpret_cast<__nv_bfloat16*>(out_lo), ld_out};
-  dim3 grid(num_segs, heads, (max_nq + kAQ - 1) / kAQ);
   cudaStream_t st = as_stream(stream);
+  const bool aligned = (ldq % 8 == 0) && (ld_local % 8 == 0) && (ld_remote % 8 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k_local) |
+                         reinterpret_cast<uintptr_t>(v_local) |
+                         reinterpret_cast<uintptr_t>(k_remote) |
+                         reinterpret_cast<uintptr_t>(v_remote)) & 15) == 0;
+  if (in_bf16 && head_dim == 64 && out_lo == nullptr && aligned && !g_force_simt_attention) {
+    static bool configured = false;
+    if (!configured) {
+      ASTRA_CUDA_CHECK(cudaFuncSetAttribute(attention_tc_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+      configured = true;
+    }
+    dim3 tgrid(num_segs, heads, (max_nq + kTQ - 1) / kTQ);
+    attention_tc_kernel<<<tgrid, 128, kTcSmem, st>>>(a);
+    ASTRA_CUDA_CHECK(cudaGetLastError());
+    return ASTRA_OK;
+  }
+  dim3 grid(num_segs, heads, (max_nq + kAQ - 1) / kAQ);
   int rc = ASTRA_OK;
   switch (head_dim) {
+    case 4: rc = launch_attn<4>(a, grid, st); break;
     case 8: rc = launch_attn<8>(a, grid, st); break;
     case 16: rc = launch_attn<16>(a, grid, st); break;
     case 32: rc = launch_attn<32>(a, grid, st); break;
@@ -218,4 +458,43 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
   if (rc) return rc;
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
+}
+
+extern "C" int astra_attention_force_simt(int enable) {
+  g_force_simt_attention = enable != 0;
+  return ASTRA_OK;
+}
+
+// Dense-mask multi-head attention for the drop-in operator API
+// (attention.multihead_attention, attention.py:50-73): one segment, fp32 in/out.
+extern "C" int astra_attention_masked(const float* q, const float* k, const float* v, int R, int C,
+                                      int D, int heads, const uint8_t* mask, int32_t* scratch,
+                                      float* out, void* stream) {
+  ASTRA_REQUIRE(heads >= 1 && D % heads == 0, ASTRA_ERR_SHAPE, "width %d not divisible by %d heads",
+                D, heads);
+  const int dk = D / heads;
+  ASTRA_REQUIRE(dk == 4 || dk == 8 || dk == 16 || dk == 32 || dk == 64 || dk == 128, ASTRA_ERR_SHAPE,
+                "attention: head_dim %d unsupported", dk);
+  if (R == 0) return ASTRA_OK;
+  std::vector<int32_t> h(6 + 2 * (size_t)C);
+  h[0] = 0; h[1] = R; h[2] = 0; h[3] = R; h[4] = 0; h[5] = C;
+  for (int j = 0; j < C; ++j) {
+    h[6 + j] = j;
+    h[6 + C + j] = j;
+  }
+  cudaStream_t st = as_stream(stream);
+  ASTRA_CUDA_CHECK(cudaMemcpyAsync(scratch, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
+  AttnArgs a{q, D, k, v, D, k, v, D, scratch + 6, scratch + 6 + C, scratch, 1, heads, dk, 0, 0,
+             (float)(1.0 / sqrt((double)dk)), out, nullptr, nullptr, D, mask, C};
+  dim3 grid(1, heads, (R + kAQ - 1) / kAQ);
+  int rc;
+  switch (dk) {
+    case 4: rc = launch_attn<4>(a, grid, st); break;
+    case 8: rc = launch_attn<8>(a, grid, st); break;
+    case 16: rc = launch_attn<16>(a, grid, st); break;
+    case 32: rc = launch_attn<32>(a, grid, st); break;
+    case 64: rc = launch_attn<64>(a, grid, st); break;
+    default: rc = launch_attn<128>(a, grid, st); break;
+  }
+  return rc;
 }

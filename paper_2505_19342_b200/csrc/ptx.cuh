@@ -139,6 +139,29 @@ ASTRA_DEVICE uint64_t sdesc_kmajor_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// MN-major, 128-byte swizzle: 64 MN elements (128 B) per row, consecutive K rows 128 B apart,
+// 8-row K groups 1024 B apart (SBO); LBO = stride between 64-wide MN blocks.
+ASTRA_DEVICE uint64_t sdesc_mnmajor_sw128(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Byte offset of 16-byte chunk `c` (0..7) of row `r` inside a 128B-swizzled tile
+// (the TMA SWIZZLE_128B / UMMA SW128 pattern; tile base 1024-byte aligned).
+ASTRA_DEVICE uint32_t sw128_offset(uint32_t r, uint32_t c) {
+  return r * 128u + ((c ^ (r & 7u)) << 4);
+}
+
+ASTRA_DEVICE void cp_async16(uint32_t smem_addr, const void* gptr) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+ASTRA_DEVICE void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // 32 lanes x 32 columns of 32-bit TMEM -> 32 registers per thread.
 ASTRA_DEVICE void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(

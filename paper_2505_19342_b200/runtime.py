@@ -80,7 +80,7 @@ class AstraRuntime:
         self.comm = comm
         self.D, self.H, self.L = cfg.hidden, cfg.heads, cfg.layers
         self.dk = cfg.hidden // cfg.heads
-        if self.dk not in (8, 16, 32, 64, 128):
+        if self.dk not in (4, 8, 16, 32, 64, 128):
             raise ShapeError(f"head_dim {self.dk} unsupported")
         self.T, self.N = plan.tokens, plan.devices
         self.G, self.K = cfg.groups, cfg.codebook_size

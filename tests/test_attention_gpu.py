@@ -1,0 +1,123 @@
+"""Mixed-precision attention kernels (tcgen05 bf16 and fp32 SIMT) vs a PyTorch fp32
+reference of the same op: segments with local and remote (codebook-table) keys,
+class-replica keys, causal masks."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(seed, segs_spec, heads=12, dk=64, causal=False, dtype=torch.bfloat16):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    D = heads * dk
+    n_local = sum(nq for nq, _, _ in segs_spec) + 8
+    qkv = (torch.randn(n_local, 3 * D, device="cuda", generator=g)).to(dtype)
+    table = (torch.randn(300, 2 * D, device="cuda", generator=g)).to(dtype)
+    rng = np.random.default_rng(seed)
+    segs, key_src, key_pos = [], [], []
+    q0 = 0
+    for nq, nk, nrep in segs_spec:
+        k0 = len(key_src)
+        ncontent = nq - nrep
+        for j in range(nk):
+            if j < nk - nrep:
+                if rng.random() < 0.5:
+                    key_src.append(int(q0 + rng.integers(0, nq)))
+                else:
+                    key_src.append(-int(rng.integers(0, 300)) - 1)
+                key_pos.append(j)
+            else:
+                key_src.append(q0 + nq - 1)
+                key_pos.append(-1)
+        segs.append([q0, nq, 5, ncontent, k0, nk])
+        q0 += nq
+    t = lambda a: torch.tensor(np.asarray(a, np.int32), device="cuda")  # noqa: E731
+    return qkv, table, t(np.asarray(segs).reshape(-1)), t(key_src), t(key_pos), segs
+
+
+def _reference(qkv, table, segs, key_src, key_pos, heads, dk, causal):
+    D = heads * dk
+    q_all, k_loc, v_loc = qkv[:, :D].float(), qkv[:, D:2 * D].float(), qkv[:, 2 * D:].float()
+    k_rem, v_rem = table[:, :D].float(), table[:, D:].float()
+    out = torch.zeros(qkv.shape[0], D, device="cuda")
+    ks, kp = key_src.cpu().numpy(), key_pos.cpu().numpy()
+    for q0, nq, qpos0, ncontent, k0, nk in segs:
+        src = ks[k0:k0 + nk]
+        pos = torch.tensor(kp[k0:k0 + nk], device="cuda")
+        loc = torch.tensor(src >= 0, device="cuda")
+        li = torch.tensor(np.where(src >= 0, src, 0), device="cuda").long()
+        ri = torch.tensor(np.where(src < 0, -(src + 1), 0), device="cuda").long()
+        K = torch.where(loc[:, None], k_loc[li], k_rem[ri])
+        V = torch.where(loc[:, None], v_loc[li], v_rem[ri])
+        qpos = torch.tensor([qpos0 + i if i < ncontent else 2 ** 31 - 1 for i in range(nq)],
+                            device="cuda")
+        mask = (pos[None, :] <= qpos[:, None]) if causal else torch.ones(nq, nk, dtype=torch.bool,
+                                                                          device="cuda")
+        for h in range(heads):
+            s = slice(h * dk, (h + 1) * dk)
+            logits = (q_all[q0:q0 + nq, s] @ K[:, s].T) * (1.0 / math.sqrt(dk))
+            logits = logits.masked_fill(~mask, float("-inf"))
+            out[q0:q0 + nq, s] = torch.softmax(logits, dim=1) @ V[:, s]
+    return out
+
+
+def test_dropin_multihead_attention_golden(cuda):
+    """attention.multihead_attention vs the reference's own outputs (test_attention.py:50: 1e-6)."""
+    from pathlib import Path
+
+    from paper_2505_19342_b200 import attention
+    from tests.golden.cases import ATT_CASES, att_case_inputs
+    gold = np.load(Path(__file__).resolve().parent / "golden" / "golden_attention.npz")
+    for i, (r, c, d, h, p) in enumerate(ATT_CASES):
+        q, k, v, mask = att_case_inputs(i, r, c, d, p)
+        out = attention.multihead_attention(q, k, v, mask, h)
+        np.testing.assert_allclose(out, gold[f"c{i}_out"], atol=1e-5)
+
+
+def test_dropin_attention_errors(cuda):
+    from paper_2505_19342_b200 import attention
+    from paper_2505_19342_b200.errors import MaskError, ShapeError
+    q = np.ones((4, 8), np.float32)
+    with pytest.raises(ShapeError):
+        attention.multihead_attention(q, q, q, np.ones((4, 4), bool), 3)
+    m = np.ones((4, 4), bool)
+    m[2] = False
+    with pytest.raises(MaskError):
+        attention.multihead_attention(q, q, q, m, 2)
+
+
+SPECS = [[(197, 197, 1)], [(50, 197, 1), (49, 197, 1), (25, 197, 1)], [(130, 300, 0), (7, 7, 0)],
+         [(256, 129, 1)]]
+
+
+@pytest.mark.parametrize("spec", SPECS)
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_attention_kernels_vs_torch(cuda, spec, causal, force_simt):
+    from paper_2505_19342_b200 import _native
+    heads, dk = 12, 64
+    qkv, table, segs_t, ks, kp, segs = _problem(len(spec) + 7 * causal, spec, heads, dk, causal)
+    D = heads * dk
+    out = torch.zeros(qkv.shape[0], D, dtype=torch.bfloat16, device="cuda")
+    lib = _native.load()
+    lib.astra_attention_force_simt(int(force_simt))
+    try:
+        es = qkv.element_size()
+        _native.call("astra_attention", qkv.data_ptr(), 3 * D, qkv.data_ptr() + D * es,
+                     qkv.data_ptr() + 2 * D * es, 3 * D, table.data_ptr(),
+                     table.data_ptr() + D * es, 2 * D, ks.data_ptr(), kp.data_ptr(),
+                     segs_t.data_ptr(), len(segs), max(s[1] for s in segs), heads, dk, int(causal),
+                     1, float(np.float32(1 / math.sqrt(dk))), None, out.data_ptr(), None, D,
+                     torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+    finally:
+        lib.astra_attention_force_simt(0)
+    ref = _reference(qkv, table, segs, ks, kp, heads, dk, causal)
+    rows = torch.cat([torch.arange(s[0], s[0] + s[1]) for s in segs]).cuda()
+    err = (out.float()[rows] - ref[rows]).abs().max().item()
+    tol = 2e-2 if not force_simt else 8e-3   # bf16 P (tcgen05) / bf16 output rounding (SIMT)
+    assert err < tol, err
