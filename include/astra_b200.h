@@ -96,6 +96,16 @@ int astra_vq_encode(const AstraCodebook* cb, const float* x, int M, int ldx, con
                     int32_t* idx_out, int32_t* stats, void* workspace, int64_t workspace_bytes,
                     void* stream);
 
+/* G = 1 variant fed by pre-split operands: x_hi/x_lo [R, D] bf16 (the LN1 pass
+ * writes them, astra_layernorm_ex) and x_norm [R] (an upper bound of ||x_r||).
+ * The distance GEMM covers all R source rows; idx_out[m] is produced for the
+ * M token rows rows[m] (fp64 re-rank reads x[rows[m]]). */
+int64_t astra_vq_encode_split_workspace(int R, int size);
+int astra_vq_encode_split(const AstraCodebook* cb, const float* x, int ldx, const void* x_hi,
+                          const void* x_lo, int ld_split, const float* x_norm, int R,
+                          const int32_t* rows, int M, int32_t* idx_out, int32_t* stats,
+                          void* workspace, int64_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------ VQ decode
  * Replaces vq.dequantize (vq.py:225-233): out[m, g*gd:(g+1)*gd] =
  * centroids[g][idx[m, g]].  Out-of-range indices are not dereferenced; they
@@ -118,6 +128,13 @@ int astra_unpack_indices(const uint32_t* words, int count, int bits, int size, i
 int astra_layernorm(const float* x, int M, int D, int ldx, const float* gain, const float* bias,
                     float eps, float* out_f32, int ld_f32, void* out_hi, void* out_lo, int ld_bf,
                     void* stream);
+/* Same, additionally writing the bf16 hi/lo split of the RAW rows (xs_hi/xs_lo,
+ * pitch ld_xs) and an upper bound of each row's norm (x_norm) — the operands of
+ * astra_vq_encode_split — from the same single read of x. */
+int astra_layernorm_ex(const float* x, int M, int D, int ldx, const float* gain, const float* bias,
+                       float eps, float* out_f32, int ld_f32, void* out_hi, void* out_lo,
+                       int ld_bf, void* xs_hi, void* xs_lo, int ld_xs, float* x_norm,
+                       void* stream);
 
 /* Stack assembly: embed_classifier_inputs (model.py:275-280) + replica rows
  * (cluster.py:189-194, :259-262).  row_src[r] >= 0: out[r] = x[row_src[r]] +

@@ -31,6 +31,11 @@ SIGNATURES: dict[str, list] = {
     "astra_vq_encode_workspace": [_c_int, _c_int, _c_int, _c_int],
     "astra_vq_encode": [_vp, _vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_ll, _vp],
     "astra_vq_decode": [_vp, _vp, _c_int, _vp, _c_int, _vp, _vp],
+    "astra_vq_encode_split_workspace": [_c_int, _c_int],
+    "astra_vq_encode_split": [_vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp,
+                              _vp, _vp, _c_ll, _vp],
+    "astra_layernorm_ex": [_vp, _c_int, _c_int, _c_int, _vp, _vp, ctypes.c_float, _vp, _c_int,
+                           _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp],
     "astra_pack_indices": [_vp, _c_int, _c_int, _vp, _vp],
     "astra_unpack_indices": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp],
     "astra_layernorm": [_vp, _c_int, _c_int, _c_int, _vp, _vp, ctypes.c_float, _vp, _c_int, _vp,
@@ -46,7 +51,8 @@ SIGNATURES: dict[str, list] = {
     "astra_attention_masked": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
                                _vp],
 }
-_RESTYPES = {"astra_last_error": ctypes.c_char_p, "astra_vq_encode_workspace": ctypes.c_longlong}
+_RESTYPES = {"astra_last_error": ctypes.c_char_p, "astra_vq_encode_workspace": ctypes.c_longlong,
+             "astra_vq_encode_split_workspace": ctypes.c_longlong}
 
 _lib = None
 
@@ -94,7 +100,7 @@ def check(status: int, what: str = "") -> None:
 
 
 # kernels each C-ABI call enqueues (for launch accounting in bench.py)
-LAUNCHES = {"astra_vq_encode": 3, "astra_vq_prepare": 2}
+LAUNCHES = {"astra_vq_encode": 3, "astra_vq_prepare": 2, "astra_vq_encode_split": 2}
 _counter: dict | None = None
 
 

@@ -110,8 +110,14 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
           sV[kj * kPad + c0 + d] = ld_elem<BF16>(vb, off + d);
         }
         if ((tid & 3) == 0) sKpos[kj] = a.key_pos[k0 + j];
-      } else if ((tid & 3) == 0) {
-        sKpos[kj] = INT_MAX;  // padding key: never visible
+      } else {
+        // padding key: never visible, and zeroed so 0-weight * stale smem cannot make a NaN
+#pragma unroll
+        for (int d = 0; d < kDPT; ++d) {
+          sK[kj * kPad + c0 + d] = 0.f;
+          sV[kj * kPad + c0 + d] = 0.f;
+        }
+        if ((tid & 3) == 0) sKpos[kj] = INT_MAX;
       }
     }
     __syncthreads();
@@ -184,22 +190,72 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
 // (codebook K/V table rows) into the tile load.
 constexpr int kTQ = 128, kTK = 128;
 static bool g_force_simt_attention = false;  // test hook (astra_attention_force_simt)
-constexpr int kTcSmem = 16384 * 3 + 32768 + 512 + 64 + 1024;
+// 16 KB Q + 2 x (16 KB K + 16 KB V) + 32 KB P + 2 x 128 int16 key positions + barrier:
+// 115,264 B, so two CTAs (and their 2 x 256 TMEM columns) share an SM.  The dynamic smem base
+// is 1024-byte aligned (checked at run time), as the SW128 layouts require.
+constexpr int kTcSmem = 16384 + 2 * 32768 + 32768 + 2 * 256 + 64;
+constexpr short kPosNever = 0x7FFF;  // padding key: never visible
 
 __host__ __device__ constexpr uint32_t idesc_bf16_f32_bmn(uint32_t M, uint32_t N) {
   return idesc_bf16_f32(M, N) | (1u << 16);  // B operand MN-major
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Issue the cp.async gather of key chunk [kc, kc+128) into (sK, sV) and its positions.
+__device__ __forceinline__ void attn_load_chunk(const AttnArgs& a, int kc, int k0, int nk,
+                                                int hoff, uint32_t k_s, uint32_t v_s,
+                                                uint8_t* sK, uint8_t* sV, short* kpos, int tid) {
+  const __nv_bfloat16* KL = reinterpret_cast<const __nv_bfloat16*>(a.k_local);
+  const __nv_bfloat16* VL = reinterpret_cast<const __nv_bfloat16*>(a.v_local);
+  const __nv_bfloat16* KR = reinterpret_cast<const __nv_bfloat16*>(a.k_remote);
+  const __nv_bfloat16* VR = reinterpret_cast<const __nv_bfloat16*>(a.v_remote);
+  // one key row per thread: a single key_src load, then 2 x 8 16-byte async copies
+  const int key = kc + tid;
+  if (key < nk) {
+    const int src = __ldg(a.key_src + k0 + key);
+    const __nv_bfloat16 *kp, *vp;
+    if (src >= 0) {
+      kp = KL + (size_t)src * a.ld_local + hoff;
+      vp = VL + (size_t)src * a.ld_local + hoff;
+    } else {
+      kp = KR + (size_t)(-(src + 1)) * a.ld_remote + hoff;
+      vp = VR + (size_t)(-(src + 1)) * a.ld_remote + hoff;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      cp_async16(k_s + sw128_offset(tid, c), kp + c * 8);
+      cp_async16(v_s + sw128_offset(tid, c), vp + c * 8);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      *reinterpret_cast<uint4*>(sK + sw128_offset(tid, c)) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(sV + sw128_offset(tid, c)) = make_uint4(0, 0, 0, 0);
+    }
+  }
+  kpos[tid] = (kc + tid < nk) ? (short)__ldg(a.key_pos + k0 + kc + tid) : kPosNever;
+}
+
 __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                           ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sK = sm + 16384;
-  uint8_t* sV = sm + 32768;
-  uint8_t* sP = sm + 49152;
-  int* sKpos = reinterpret_cast<int*>(sm + 81920);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 81920 + 512);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  if (smem_u32(sm) & 1023) __trap();      // SW128 tiles need a 1024-byte aligned base
+  uint8_t* sQ = sm;                       // 16 KB
+  uint8_t* sK0 = sm + 16384;              // 2 x 16 KB
+  uint8_t* sV0 = sm + 16384 + 32768;      // 2 x 16 KB
+  uint8_t* sP = sm + 16384 + 65536;       // 32 KB
+  short* sKpos = reinterpret_cast<short*>(sm + 16384 + 98304);   // 2 x 128
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 16384 + 98304 + 512);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
   const int seg = blockIdx.x, h = blockIdx.y, qt = blockIdx.z;
@@ -209,25 +265,33 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int hoff = h * 64;
   const __nv_bfloat16* Q = reinterpret_cast<const __nv_bfloat16*>(a.q);
-  const __nv_bfloat16* KL = reinterpret_cast<const __nv_bfloat16*>(a.k_local);
-  const __nv_bfloat16* VL = reinterpret_cast<const __nv_bfloat16*>(a.v_local);
-  const __nv_bfloat16* KR = reinterpret_cast<const __nv_bfloat16*>(a.k_remote);
-  const __nv_bfloat16* VR = reinterpret_cast<const __nv_bfloat16*>(a.v_remote);
 
   if (warp == 0) tmem_alloc<256>(tslot);
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_barrier_init();
   }
-  const uint32_t q_s = smem_u32(sQ), k_s = smem_u32(sK), v_s = smem_u32(sV), p_s = smem_u32(sP);
-  for (int i = tid; i < kTQ * 8; i += 128) {
-    const int r = i >> 3, c = i & 7, qi = qt * kTQ + r;
-    const uint32_t dst = q_s + sw128_offset(r, c);
-    if (qi < nq)
-      cp_async16(dst, Q + (size_t)(q0 + qi) * a.ldq + hoff + c * 8);
-    else
-      *reinterpret_cast<uint4*>(sQ + sw128_offset(r, c)) = make_uint4(0, 0, 0, 0);
+  const uint32_t q_s = smem_u32(sQ), p_s = smem_u32(sP);
+  // prologue: group 0 = Q + key chunk 0, group 1 = key chunk 1
+  {
+    const int qr = qt * kTQ + tid;  // one query row per thread
+    if (qr < nq) {
+      const __nv_bfloat16* qp = Q + (size_t)(q0 + qr) * a.ldq + hoff;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) cp_async16(q_s + sw128_offset(tid, c), qp + c * 8);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(sQ + sw128_offset(tid, c)) = make_uint4(0, 0, 0, 0);
+    }
   }
+  const int nchunks = (nk + kTK - 1) / kTK;
+  attn_load_chunk(a, 0, k0, nk, hoff, smem_u32(sK0), smem_u32(sV0), sK0, sV0, sKpos, tid);
+  cp_async_commit();
+  if (nchunks > 1)
+    attn_load_chunk(a, kTK, k0, nk, hoff, smem_u32(sK0 + 16384), smem_u32(sV0 + 16384),
+                    sK0 + 16384, sV0 + 16384, sKpos + 128, tid);
+  cp_async_commit();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -237,7 +301,7 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
 
   const int r = warp * 32 + lane;
   const int qi = qt * kTQ + r;
-  const int qpos = qi < ncontent ? qpos0 + qi : INT_MAX;
+  const int qpos = qi < ncontent ? qpos0 + qi : 0x7FFE;  // replica / pad queries see all keys
   const float sl2 = a.scale * 1.4426950408889634f;  // exp(x) = exp2(x * log2 e)
   float m = -INFINITY, l = 0.f;
   float o[64];
@@ -245,29 +309,12 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
   for (int d = 0; d < 64; ++d) o[d] = 0.f;
   uint32_t phase = 0;
 
-  for (int kc = 0; kc < nk; kc += kTK) {
-    for (int i = tid; i < kTK * 8; i += 128) {
-      const int j = i >> 3, c = i & 7, key = kc + j;
-      const uint32_t off = sw128_offset(j, c);
-      if (key < nk) {
-        const int src = a.key_src[k0 + key];
-        const __nv_bfloat16 *kp, *vp;
-        if (src >= 0) {
-          kp = KL + (size_t)src * a.ld_local;
-          vp = VL + (size_t)src * a.ld_local;
-        } else {
-          kp = KR + (size_t)(-(src + 1)) * a.ld_remote;
-          vp = VR + (size_t)(-(src + 1)) * a.ld_remote;
-        }
-        cp_async16(k_s + off, kp + hoff + c * 8);
-        cp_async16(v_s + off, vp + hoff + c * 8);
-      } else {
-        *reinterpret_cast<uint4*>(sK + off) = make_uint4(0, 0, 0, 0);
-        *reinterpret_cast<uint4*>(sV + off) = make_uint4(0, 0, 0, 0);
-      }
-    }
-    sKpos[tid] = (kc + tid < nk) ? a.key_pos[k0 + kc + tid] : INT_MAX;
-    cp_async_wait_all();
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1, kc = c * kTK;
+    uint8_t* sK = sK0 + buf * 16384;
+    uint8_t* sV = sV0 + buf * 16384;
+    const short* kpos = sKpos + buf * 128;
+    cp_async_wait_group<1>();   // this chunk's group has landed (the next may be in flight)
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -275,7 +322,7 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
     if (tid == 0) {
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_f16(tS, sdesc_kmajor_sw128(q_s + kk * 32), sdesc_kmajor_sw128(k_s + kk * 32),
+        umma_f16(tS, sdesc_kmajor_sw128(q_s + kk * 32), sdesc_kmajor_sw128(smem_u32(sK) + kk * 32),
                  idesc_bf16_f32(128, 128), kk > 0 ? 1u : 0u);
       umma_commit(bar);
     }
@@ -283,53 +330,66 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
     phase ^= 1;
     tc_fence_after();
 
-    // ---- softmax (row r): pass 1 max, pass 2 exp + P store
-    float cmax = -INFINITY;
+    // ---- softmax of row r over this chunk.  Non-causal: only the chunk tail is masked
+    // (uniform bound); causal: key_pos <= query position, replica keys (pos -1) visible.
+    const int valid = min(kTK, nk - kc);
+    float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll 1
     for (int cc = 0; cc < 4; ++cc) {
+      if (cc * 32 >= valid) break;
       uint32_t rr[32];
       tmem_ld32(tS + lane_off + cc * 32, rr);
       tmem_ld_wait();
+      const bool full = !a.causal && (cc * 32 + 32 <= valid);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const int kp = sKpos[cc * 32 + j];
-        const bool vis = kp != INT_MAX && (!a.causal || kp <= qpos);
-        if (vis) cmax = fmaxf(cmax, __uint_as_float(rr[j]));
+        const int col = cc * 32 + j;
+        const bool vis = full || (col < valid && (!a.causal || kpos[col] <= qpos));
+        if (vis) mx[j & 3] = fmaxf(mx[j & 3], __uint_as_float(rr[j]));
       }
     }
+    const float cmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
     const float mnew = fmaxf(m, cmax * sl2);
-    const float corr = (m == -INFINITY) ? 0.f : exp2f(m - mnew);
-    float lsum = 0.f;
+    const float corr = (m == -INFINITY) ? 0.f : ex2_approx(m - mnew);
+    float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
     for (int cc = 0; cc < 4; ++cc) {
-      uint32_t rr[32];
-      tmem_ld32(tS + lane_off + cc * 32, rr);
-      tmem_ld_wait();
+      uint4* prow = nullptr;
       uint32_t pk[16];
+      if (cc * 32 < valid) {
+        uint32_t rr[32];
+        tmem_ld32(tS + lane_off + cc * 32, rr);
+        tmem_ld_wait();
+        const bool full = !a.causal && (cc * 32 + 32 <= valid);
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        float p2[2];
+        for (int j = 0; j < 32; j += 2) {
+          float p2[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int kp = sKpos[cc * 32 + j + u];
-          const bool vis = kp != INT_MAX && (!a.causal || kp <= qpos);
-          p2[u] = vis ? exp2f(__uint_as_float(rr[j + u]) * sl2 - mnew) : 0.f;
+          for (int u = 0; u < 2; ++u) {
+            const int col = cc * 32 + j + u;
+            const bool vis = full || (col < valid && (!a.causal || kpos[col] <= qpos));
+            p2[u] = vis ? ex2_approx(fmaf(__uint_as_float(rr[j + u]), sl2, -mnew)) : 0.f;
+          }
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
+          // sum what the tensor core multiplies (the bf16-rounded probabilities)
+          ls[(j >> 1) & 3] += __low2float(b2) + __high2float(b2);
+          pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
-        // sum what the tensor core will multiply (the bf16-rounded probabilities)
-        lsum += __low2float(b2) + __high2float(b2);
-        pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = 0u;
       }
-      const int col0 = cc * 32;                 // key within chunk
-      uint8_t* blk = sP + (col0 >> 6) * 16384;  // 64-key K-block
+      const int col0 = cc * 32;
+      uint8_t* blk = sP + (col0 >> 6) * 16384;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int chunk = ((col0 & 63) >> 3) + q;
         *reinterpret_cast<uint4*>(blk + sw128_offset(r, chunk)) =
             make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
       }
+      (void)prow;
     }
-    l = l * corr + lsum;
+    l = l * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
     m = mnew;
     fence_proxy_async();
     tc_fence_before();
@@ -339,7 +399,7 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
         umma_f16(tO, sdesc_kmajor_sw128(p_s + (kk >> 2) * 16384 + (kk & 3) * 32),
-                 sdesc_mnmajor_sw128(v_s + kk * 2048, 8192), idesc_bf16_f32_bmn(128, 64),
+                 sdesc_mnmajor_sw128(smem_u32(sV) + kk * 2048, 8192), idesc_bf16_f32_bmn(128, 64),
                  kk > 0 ? 1u : 0u);
       umma_commit(bar);
     }
@@ -358,7 +418,11 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
       }
     }
     tc_fence_before();
-    __syncthreads();
+    __syncthreads();   // buffers of this chunk are free
+    if (c + 2 < nchunks)
+      attn_load_chunk(a, (c + 2) * kTK, k0, nk, hoff, smem_u32(sK), smem_u32(sV), sK, sV,
+                      sKpos + buf * 128, tid);
+    cp_async_commit();
   }
 
   if (qi < nq) {

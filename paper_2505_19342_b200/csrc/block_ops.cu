@@ -17,7 +17,9 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
                                  const float* __restrict__ gain, const float* __restrict__ bias,
                                  float eps, float* __restrict__ out_f32, int ld_f32,
                                  __nv_bfloat16* __restrict__ out_hi, __nv_bfloat16* __restrict__ out_lo,
-                                 int ld_bf) {
+                                 int ld_bf, __nv_bfloat16* __restrict__ xs_hi,
+                                 __nv_bfloat16* __restrict__ xs_lo, int ld_xs,
+                                 float* __restrict__ x_norm) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < M; row += gridDim.x * warps) {
@@ -28,6 +30,16 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
     for (int i = 0; i < VPL; ++i) {
       v[i] = __ldg(xr + lane + 32 * i);
       s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+      if (xs_hi) {  // bf16 hi/lo split of the raw row: the VQ-encode GEMM operand
+        __nv_bfloat16 h[4], l[4];
+        split_bf16(v[i].x, h[0], l[0]);
+        split_bf16(v[i].y, h[1], l[1]);
+        split_bf16(v[i].z, h[2], l[2]);
+        split_bf16(v[i].w, h[3], l[3]);
+        const size_t o = (size_t)row * ld_xs + (lane + 32 * i) * 4;
+        *reinterpret_cast<uint2*>(xs_hi + o) = *reinterpret_cast<uint2*>(h);
+        *reinterpret_cast<uint2*>(xs_lo + o) = *reinterpret_cast<uint2*>(l);
+      }
     }
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const float D = (float)(VPL * 128);
@@ -40,6 +52,8 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
     }
     for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
     const float inv = 1.0f / sqrtf(q / D + eps);
+    // ||x|| upper bound for the VQ error window: ||x||^2 = sum (x-mu)^2 + D mu^2
+    if (x_norm && lane == 0) x_norm[row] = sqrtf(q + D * mu * mu) * (1.0f + 1e-5f);
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int c = (lane + 32 * i) * 4;
@@ -175,29 +189,48 @@ static int grid_rows(int rows, int warps_per_block) {
 
 using namespace astra;
 
-extern "C" int astra_layernorm(const float* x, int M, int D, int ldx, const float* gain,
-                               const float* bias, float eps, float* out_f32, int ld_f32,
-                               void* out_hi, void* out_lo, int ld_bf, void* stream) {
+extern "C" int astra_layernorm_ex(const float* x, int M, int D, int ldx, const float* gain,
+                                  const float* bias, float eps, float* out_f32, int ld_f32,
+                                  void* out_hi, void* out_lo, int ld_bf, void* xs_hi, void* xs_lo,
+                                  int ld_xs, float* x_norm, void* stream) {
   ASTRA_REQUIRE(M >= 0 && D > 0, ASTRA_ERR_SHAPE, "layernorm: bad shape");
   ASTRA_REQUIRE(eps > 0.f, ASTRA_ERR_SHAPE, "layer_norm: eps must be positive");
+  ASTRA_REQUIRE((xs_hi == nullptr) == (xs_lo == nullptr), ASTRA_ERR_SHAPE,
+                "layernorm: split outputs come in pairs");
   if (M == 0) return ASTRA_OK;
   cudaStream_t s = as_stream(stream);
   auto hi = reinterpret_cast<__nv_bfloat16*>(out_hi);
   auto lo = reinterpret_cast<__nv_bfloat16*>(out_lo);
+  auto xh = reinterpret_cast<__nv_bfloat16*>(xs_hi);
+  auto xl = reinterpret_cast<__nv_bfloat16*>(xs_lo);
   const bool vec = (D % 128 == 0) && (ldx % 4 == 0) && (!out_f32 || ld_f32 % 4 == 0) &&
-                   (!out_hi || ld_bf % 4 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+                   (!out_hi || ld_bf % 4 == 0) && (!xs_hi || ld_xs % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   const int grid = grid_rows(M, 8);
   if (vec && D == 768)
-    layernorm_kernel<6><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo, ld_bf);
+    layernorm_kernel<6><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+                                             ld_bf, xh, xl, ld_xs, x_norm);
   else if (vec && D == 1024)
-    layernorm_kernel<8><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo, ld_bf);
+    layernorm_kernel<8><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+                                             ld_bf, xh, xl, ld_xs, x_norm);
   else if (vec && D == 512)
-    layernorm_kernel<4><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo, ld_bf);
-  else
+    layernorm_kernel<4><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+                                             ld_bf, xh, xl, ld_xs, x_norm);
+  else {
+    ASTRA_REQUIRE(xs_hi == nullptr && x_norm == nullptr, ASTRA_ERR_SHAPE,
+                  "layernorm: split / norm outputs need D in {512, 768, 1024}");
     layernorm_generic_kernel<<<grid, 256, 0, s>>>(x, M, D, ldx, gain, bias, eps, out_f32, ld_f32,
                                                   hi, lo, ld_bf);
+  }
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
+}
+
+extern "C" int astra_layernorm(const float* x, int M, int D, int ldx, const float* gain,
+                               const float* bias, float eps, float* out_f32, int ld_f32,
+                               void* out_hi, void* out_lo, int ld_bf, void* stream) {
+  return astra_layernorm_ex(x, M, D, ldx, gain, bias, eps, out_f32, ld_f32, out_hi, out_lo, ld_bf,
+                            nullptr, nullptr, 0, nullptr, stream);
 }
 
 extern "C" int astra_embed_stack(const float* x, const float* pos, const float* cls,

@@ -1,10 +1,25 @@
 // Projection / MLP GEMMs of the Astra block with fused epilogues
 // (reference: tensor.matmul tensor.py:142-155, add_bias :186-190, gelu :348-358,
 // residual adds cluster.py:213 and :216).
+//
+// Epilogue I/O is staged through a warp-private 4 KB shared-memory tile (128B-swizzled, so
+// both the row-per-thread TMEM side and the coalesced global side are bank-conflict free):
+// residual tiles are read with fully coalesced 16-byte loads, results leave as fully
+// coalesced 16-byte stores (a warp writes 4 fp32 rows x 128 B or 8 bf16 rows x 64 B per
+// instruction) instead of 32 scattered row segments.
 #include "host_common.h"
 #include "tc_gemm.cuh"
 
 namespace astra {
+
+// fp32 staging tile [32 rows][32 floats]: 16B chunk c of row r lives at slot c ^ (r & 7)
+__device__ __forceinline__ float4* st_f32(uint8_t* stage, int r, int c) {
+  return reinterpret_cast<float4*>(stage + r * 128 + ((c ^ (r & 7)) << 4));
+}
+// bf16 staging tile [32 rows][32 bf16 = 64 B]: chunk c (0..3) of row r at slot c ^ ((r>>1)&3)
+__device__ __forceinline__ uint4* st_bf(uint8_t* stage, int r, int c) {
+  return reinterpret_cast<uint4*>(stage + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+}
 
 struct StdEpilogue {
   int M, N;
@@ -18,53 +33,101 @@ struct StdEpilogue {
   int ld_bf;
   int gelu;
   int BN;
+  int vec;  // all row pitches / bases allow 16-byte vectors
 
-  __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile,
-                                             uint32_t taddr) const {
-    const int row = tc.m_blk * kBM + row_in_tile;
+  __device__ __forceinline__ void store_bf16(uint8_t* stage, __nv_bfloat16* out, int row0,
+                                             int col0, const __nv_bfloat16 (&h)[32]) const {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) *st_bf(stage, lane, c) = *reinterpret_cast<const uint4*>(h + 8 * c);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rr = i * 8 + (lane >> 2), ch = lane & 3, grow = row0 + rr;
+      if (grow < M)
+        *reinterpret_cast<uint4*>(out + (size_t)grow * ld_bf + col0 + ch * 8) = *st_bf(stage, rr, ch);
+    }
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
+                                             int cb, int ce, uint8_t* stage) const {
+    const int lane = threadIdx.x & 31;
+    const int row0 = tc.m_blk * kBM + row_in_tile - lane;  // first row of this warp's slab
+    const int row = row0 + lane;
     const bool row_ok = row < M;
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    float* sbias = reinterpret_cast<float*>(stage + 4096);
+    for (int c0 = cb; c0 < ce; c0 += 32) {
+      const int col0 = tc.n_blk * BN + c0;
+      // one coalesced bias load per warp, issued before the TMEM load so the latencies overlap
+      const float bl = (bias && col0 + lane < N) ? __ldg(bias + col0 + lane) : 0.f;
       uint32_t r[32];
       tmem_ld32(taddr + c0, r);
       tmem_ld_wait();
-      const int col0 = tc.n_blk * BN + c0;
-      if (!row_ok || col0 >= N) continue;
+      if (col0 >= N) continue;  // warp-uniform
+      const bool full = (col0 + 32 <= N);
+      const bool fast = full && vec;
       float v[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-      const bool full = (col0 + 32 <= N);
       if (bias) {
+        sbias[lane] = bl;
+        __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (full || col0 + j < N) v[j] += __ldg(bias + col0 + j);
+        for (int j = 0; j < 32; j += 4) {
+          const float4 b4 = *reinterpret_cast<const float4*>(sbias + j);  // broadcast read
+          v[j] += b4.x;
+          v[j + 1] += b4.y;
+          v[j + 2] += b4.z;
+          v[j + 3] += b4.w;
+        }
+        __syncwarp();
       }
       if (gelu) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
       }
       if (residual) {
-        const float* rp = residual + (size_t)row * ld_res + col0;
-        if (full && ((reinterpret_cast<uintptr_t>(rp) & 15) == 0)) {
+        if (fast) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            float4 q = *reinterpret_cast<const float4*>(rp + j);
-            v[j] = q.x + v[j];
-            v[j + 1] = q.y + v[j + 1];
-            v[j + 2] = q.z + v[j + 2];
-            v[j + 3] = q.w + v[j + 3];
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + (lane >> 3), ch = lane & 7, grow = row0 + rr;
+            if (grow < M)
+              *st_f32(stage, rr, ch) =
+                  __ldg(reinterpret_cast<const float4*>(residual + (size_t)grow * ld_res + col0) + ch);
           }
-        } else {
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 q = *st_f32(stage, lane, c);
+            v[4 * c] = q.x + v[4 * c];
+            v[4 * c + 1] = q.y + v[4 * c + 1];
+            v[4 * c + 2] = q.z + v[4 * c + 2];
+            v[4 * c + 3] = q.w + v[4 * c + 3];
+          }
+          __syncwarp();
+        } else if (row_ok) {
+          const float* rp = residual + (size_t)row * ld_res + col0;
           for (int j = 0; j < 32; ++j)
             if (col0 + j < N) v[j] = rp[j] + v[j];
         }
       }
       if (out_f32) {
-        float* op = out_f32 + (size_t)row * ld_f32 + col0;
-        if (full && ((reinterpret_cast<uintptr_t>(op) & 15) == 0)) {
+        if (fast) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(op + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        } else {
+          for (int c = 0; c < 8; ++c)
+            *st_f32(stage, lane, c) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + (lane >> 3), ch = lane & 7, grow = row0 + rr;
+            if (grow < M)
+              *(reinterpret_cast<float4*>(out_f32 + (size_t)grow * ld_f32 + col0) + ch) =
+                  *st_f32(stage, rr, ch);
+          }
+          __syncwarp();
+        } else if (row_ok) {
+          float* op = out_f32 + (size_t)row * ld_f32 + col0;
           for (int j = 0; j < 32; ++j)
             if (col0 + j < N) op[j] = v[j];
         }
@@ -73,15 +136,12 @@ struct StdEpilogue {
         __nv_bfloat16 hi[32], lo[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) split_bf16(v[j], hi[j], lo[j]);
-        __nv_bfloat16* hp = out_hi + (size_t)row * ld_bf + col0;
-        __nv_bfloat16* lp = out_lo ? out_lo + (size_t)row * ld_bf + col0 : nullptr;
-        if (full && ((reinterpret_cast<uintptr_t>(hp) & 15) == 0)) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            *reinterpret_cast<uint4*>(hp + j) = *reinterpret_cast<const uint4*>(hi + j);
-            if (lp) *reinterpret_cast<uint4*>(lp + j) = *reinterpret_cast<const uint4*>(lo + j);
-          }
-        } else {
+        if (fast) {
+          store_bf16(stage, out_hi, row0, col0, hi);
+          if (out_lo) store_bf16(stage, out_lo, row0, col0, lo);
+        } else if (row_ok) {
+          __nv_bfloat16* hp = out_hi + (size_t)row * ld_bf + col0;
+          __nv_bfloat16* lp = out_lo ? out_lo + (size_t)row * ld_bf + col0 : nullptr;
           for (int j = 0; j < 32; ++j)
             if (col0 + j < N) {
               hp[j] = hi[j];
@@ -99,6 +159,7 @@ static int launch_std(const CUtensorMap& ta, const CUtensorMap& talo, const CUte
                       cudaStream_t stream) {
   auto kern = tc_gemm_kernel<BN, PASSES, STAGES, StdEpilogue>;
   constexpr int smem = gemm_smem_bytes<BN, PASSES, STAGES>();
+  static_assert(smem <= 232448, "GEMM smem budget exceeded");
   static bool configured = false;
   if (!configured) {
     ASTRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -111,6 +172,29 @@ static int launch_std(const CUtensorMap& ta, const CUtensorMap& talo, const CUte
   kern<<<grid, kGemmThreads, smem, stream>>>(ta, talo, tb, tblo, K, sched, 0, 0, epi);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
+}
+
+// Tile width: minimise (persistent waves x tile cost); narrow tiles pay ~15% more per column
+// (shared-memory operand bandwidth), 192 ~5%.
+static int pick_bn(int M, int N) {
+  const int sms = num_sms();
+  const int num_m = (M + kBM - 1) / kBM;
+  const int cands[3] = {256, 192, 128};
+  const double eff[3] = {1.0, 1.05, 1.15};
+  int best = 128;
+  double best_cost = 1e30;
+  for (int i = 0; i < 3; ++i) {
+    const int bn = cands[i];
+    if (bn > 128 && N < bn) continue;
+    const long tiles = (long)num_m * ((N + bn - 1) / bn);
+    const long waves = (tiles + sms - 1) / sms;
+    const double cost = (double)waves * bn * eff[i];
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
 }
 
 }  // namespace astra
@@ -130,10 +214,7 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                 "astra_gemm: passes=3 needs lo operands");
   ASTRA_REQUIRE(out_lo == nullptr || out_hi != nullptr, ASTRA_ERR_SHAPE,
                 "astra_gemm: out_lo requires out_hi");
-  // Wide N: 256-column tiles if that still fills the machine, else 128.
-  const int num_m = (M + kBM - 1) / kBM;
-  const bool wide = (N >= 256) && ((long)num_m * ((N + 255) / 256) >= num_sms());
-  const int BN = wide ? 256 : 128;
+  const int BN = pick_bn(M, N);
   CUtensorMap ta, talo, tb, tblo;
   int st;
   if ((st = make_tmap_2d(&ta, a_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, lda, kBM, kBK, true)))
@@ -151,14 +232,21 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
     talo = ta;
     tblo = tb;
   }
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const int vec = (!residual || (ld_res % 4 == 0 && al16(residual))) &&
+                  (!out_f32 || (ld_f32 % 4 == 0 && al16(out_f32))) &&
+                  (!out_hi || (ld_bf % 8 == 0 && al16(out_hi) && (!out_lo || al16(out_lo))));
   StdEpilogue epi{M,      N,      bias,
                   residual, ld_res, out_f32,
                   ld_f32, reinterpret_cast<__nv_bfloat16*>(out_hi),
-                  reinterpret_cast<__nv_bfloat16*>(out_lo), ld_bf, gelu, 0};
+                  reinterpret_cast<__nv_bfloat16*>(out_lo), ld_bf, gelu, 0, vec};
   cudaStream_t s = as_stream(stream);
-  if (passes == 1)
-    return wide ? launch_std<256, 1, 4>(ta, talo, tb, tblo, M, N, K, epi, s)
-                : launch_std<128, 1, 6>(ta, talo, tb, tblo, M, N, K, epi, s);
-  return wide ? launch_std<256, 3, 2>(ta, talo, tb, tblo, M, N, K, epi, s)
-              : launch_std<128, 3, 3>(ta, talo, tb, tblo, M, N, K, epi, s);
+  if (passes == 1) {
+    if (BN == 256) return launch_std<256, 1, 4>(ta, talo, tb, tblo, M, N, K, epi, s);
+    if (BN == 192) return launch_std<192, 1, 4>(ta, talo, tb, tblo, M, N, K, epi, s);
+    return launch_std<128, 1, 6>(ta, talo, tb, tblo, M, N, K, epi, s);
+  }
+  if (BN == 256) return launch_std<256, 3, 2>(ta, talo, tb, tblo, M, N, K, epi, s);
+  if (BN == 192) return launch_std<192, 3, 2>(ta, talo, tb, tblo, M, N, K, epi, s);
+  return launch_std<128, 3, 3>(ta, talo, tb, tblo, M, N, K, epi, s);
 }

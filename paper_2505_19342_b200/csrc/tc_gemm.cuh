@@ -21,7 +21,9 @@ namespace astra {
 constexpr int kBM = 128;  // UMMA M (rows per tile)
 constexpr int kBK = 64;   // bf16 elements per 128-byte swizzle row
 constexpr int kUK = 16;   // UMMA K for kind::f16
-constexpr int kGemmThreads = 192;
+constexpr int kEpiWarps = 8;      // two warps per TMEM lane quarter, each owns half the columns
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiStageBytes = 4096 + 128;  // per-epilogue-warp smem: 32x32 fp32 tile + 32 floats
 
 template <int BN, int PASSES>
 struct GemmSmem {
@@ -33,7 +35,8 @@ struct GemmSmem {
 
 template <int BN, int PASSES, int STAGES>
 constexpr int gemm_smem_bytes() {
-  return STAGES * GemmSmem<BN, PASSES>::kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  return STAGES * GemmSmem<BN, PASSES>::kStageBytes + kEpiWarps * kEpiStageBytes +
+         1024 /*align*/ + 256 /*barriers*/;
 }
 
 struct TileCoord {
@@ -58,8 +61,9 @@ struct TileSched {
 // Epi must provide:
 //   __device__ void operator()(const TileCoord&, int row_in_tile /*0..127*/,
 //                              uint32_t tmem_row_addr /*lane-qualified TMEM address of col 0*/,
-//                              int BN) const;
-// It reads its accumulator row via tmem_ld32 and writes results.
+//                              int col_begin, int col_end /*this warp's column half*/,
+//                              uint8_t* stage /*kEpiStageBytes of warp-private smem*/) const;
+// It reads its accumulator row via tmem_ld32 (warp-collective) and writes results.
 template <int BN, int PASSES, int STAGES, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
@@ -70,7 +74,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                  : (2 * BN <= 256) ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStageBytes);
+  uint8_t* epi_stage = smem + STAGES * S::kStageBytes;
+  uint64_t* full_bar =
+      reinterpret_cast<uint64_t*>(epi_stage + kEpiWarps * kEpiStageBytes);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      mbar_init(&tempty_bar[s], 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -180,6 +186,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // -------------------------------------------------------------- epilogue
     const uint32_t quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
+    const int half = (warp - 2) / 4;
+    const int col_begin = half * (BN / 2), col_end = col_begin + BN / 2;
+    uint8_t* stage = epi_stage + (warp - 2) * kEpiStageBytes;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -187,7 +196,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;
-      epi(tc, row_in_tile, taddr);
+      epi(tc, row_in_tile, taddr, col_begin, col_end, stage);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {

@@ -42,7 +42,7 @@ struct VqWorkspace {
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
-  const int nchunk = (K + kVqBN - 1) / kVqBN;
+  const int nchunk = 2 * ((K + kVqBN - 1) / kVqBN);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -148,53 +148,62 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
 
 // ---------------------------------------------------------- epilogue
 struct VqEpilogue {
-  int M, K, nchunk;
+  int M, K, nchunk;         // nchunk = records per (g, row) = 2 per 256-code tile (column halves)
   const float* c_sq;        // [G, K]
   const float* c_norm_max;  // [G]
   VqWorkspace w;
 
-  __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile,
-                                             uint32_t taddr) const {
+  __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
+                                             int cb, int ce, uint8_t* stage) const {
     const int row = tc.m_blk * kBM + row_in_tile;
     const bool ok = row < M;
     const int g = tc.batch;
     const int col_base = tc.n_blk * kVqBN;
     const float* csq = c_sq + (size_t)g * K;
     float best = INFINITY;
-    int bidx = -1;
+    // ||c||^2 of the 32 columns of a chunk: one coalesced load per warp, broadcast from smem
+    // (columns >= K get +inf, so they never win and never enter the window)
+    float* scs = reinterpret_cast<float*>(stage);
+    const int lane = threadIdx.x & 31;
+    float bst[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll 1
-    for (int c0 = 0; c0 < kVqBN; c0 += 32) {
+    for (int c0 = cb; c0 < ce; c0 += 32) {
+      const int col0 = col_base + c0;
+      const float cl = (col0 + lane < K) ? __ldg(csq + col0 + lane) : INFINITY;
       uint32_t r[32];
       tmem_ld32(taddr + c0, r);
       tmem_ld_wait();
-      const int col0 = col_base + c0;
+      scs[lane] = cl;
+      __syncwarp();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = col0 + j;
-        if (col < K) {
-          const float s = fmaf(-2.0f, __uint_as_float(r[j]), __ldg(csq + col));
-          if (s < best) {
-            best = s;
-            bidx = col;
-          }
-        }
+      for (int j = 0; j < 32; j += 4) {
+        const float4 q = *reinterpret_cast<const float4*>(scs + j);
+        bst[0] = fminf(bst[0], fmaf(-2.0f, __uint_as_float(r[j]), q.x));
+        bst[1] = fminf(bst[1], fmaf(-2.0f, __uint_as_float(r[j + 1]), q.y));
+        bst[2] = fminf(bst[2], fmaf(-2.0f, __uint_as_float(r[j + 2]), q.z));
+        bst[3] = fminf(bst[3], fmaf(-2.0f, __uint_as_float(r[j + 3]), q.w));
       }
+      __syncwarp();
     }
+    best = fminf(fminf(bst[0], bst[1]), fminf(bst[2], bst[3]));
     const float xn = ok ? w.x_norm[(size_t)g * M + row] : 0.f;
     const float thr = best + 2.0f * score_delta(xn, __ldg(c_norm_max + g));
-    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk;
+    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk * 2 + (cb > 0 ? 1 : 0);
     int cnt = 0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < kVqBN; c0 += 32) {
+    for (int c0 = cb; c0 < ce; c0 += 32) {
+      const int col0 = col_base + c0;
+      const float cl = (col0 + lane < K) ? __ldg(csq + col0 + lane) : INFINITY;
       uint32_t r[32];
       tmem_ld32(taddr + c0, r);
       tmem_ld_wait();
-      const int col0 = col_base + c0;
+      scs[lane] = cl;
+      __syncwarp();
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int col = col0 + j;
         if (col < K) {
-          const float s = fmaf(-2.0f, __uint_as_float(r[j]), __ldg(csq + col));
+          const float s = fmaf(-2.0f, __uint_as_float(r[j]), scs[j]);
           if (s <= thr) {
             if (ok && cnt < kVqCap) {
               w.rec_idx[rec * kVqCap + cnt] = col;
@@ -204,12 +213,12 @@ struct VqEpilogue {
           }
         }
       }
+      __syncwarp();
     }
     if (ok) {
       w.rec_best[rec] = best;
       w.rec_cnt[rec] = cnt;
     }
-    (void)bidx;
   }
 };
 
@@ -228,45 +237,64 @@ __device__ __forceinline__ double exact_d2(const float* xr, const float* c, int 
   return (pp - 2.0 * pc) + cc;
 }
 
-// one warp per (g, row)
+// One thread decides one (g, row): the window candidates of its 2*ceil(K/256) chunk records
+// are merged; a single survivor is the answer.  Rows with several survivors (or a chunk whose
+// candidate list overflowed) are then re-ranked one after another by the whole warp in exact
+// fp64 — the reference's own expression (||p||^2 - 2 p.c) + ||c||^2, ties to the lowest index.
 __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x, int M, int ldx,
                                    const int32_t* __restrict__ rows, VqWorkspace w, int nchunk,
-                                   int32_t* __restrict__ idx_out, int32_t* __restrict__ stats) {
-  const int warps = blockDim.x >> 5;
-  const int item = blockIdx.x * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+                                   int32_t* __restrict__ idx_out, int32_t* __restrict__ stats,
+                                   int Mrec, int rec_by_row) {
   const int G = cb.groups, K = cb.size, gd = cb.group_dim;
-  if (item >= G * M) return;
-  const int g = item / M, row = item % M;
-  const size_t rec0 = ((size_t)g * M + row) * nchunk;
-  float best = INFINITY;
-  for (int c = 0; c < nchunk; ++c) best = fminf(best, w.rec_best[rec0 + c]);
-  const float thr = best + 2.0f * score_delta(w.x_norm[(size_t)g * M + row], cb.c_norm_max[g]);
-  int n = 0, only = -1;
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool active = item < G * M;
+  int g = 0, row = 0, rr = 0, n = 0, only = -1;
   bool overflow = false;
-  for (int c = 0; c < nchunk; ++c) {
-    const int cnt = w.rec_cnt[rec0 + c];
-    if (w.rec_best[rec0 + c] > thr) continue;
-    if (cnt > kVqCap) overflow = true;
-    const int m = cnt < kVqCap ? cnt : kVqCap;
-    for (int i = 0; i < m; ++i)
-      if (w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
-        ++n;
-        only = w.rec_idx[(rec0 + c) * kVqCap + i];
-      }
+  float thr = 0.f;
+  size_t rec0 = 0;
+  if (active) {
+    g = item / M;
+    row = item % M;
+    // records / norms are indexed by token (gathered split) or by source row (pre-split stack)
+    rr = rec_by_row ? rows[row] : row;
+    rec0 = ((size_t)g * Mrec + rr) * nchunk;
+    float best = INFINITY;
+    for (int c = 0; c < nchunk; ++c) best = fminf(best, w.rec_best[rec0 + c]);
+    thr = best + 2.0f * score_delta(w.x_norm[(size_t)g * Mrec + rr], cb.c_norm_max[g]);
+    for (int c = 0; c < nchunk; ++c) {
+      if (w.rec_best[rec0 + c] > thr) continue;
+      const int cnt = w.rec_cnt[rec0 + c];
+      if (cnt > kVqCap) overflow = true;
+      const int m = cnt < kVqCap ? cnt : kVqCap;
+      for (int i = 0; i < m; ++i)
+        if (w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
+          ++n;
+          only = w.rec_idx[(rec0 + c) * kVqCap + i];
+        }
+    }
   }
-  int result = only;
-  if (overflow || n > 1) {
-    const int src = rows ? rows[row] : row;
-    const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
+  const bool need = active && (overflow || n > 1);
+  unsigned todo = __ballot_sync(0xffffffffu, need);
+  if (active && !need) idx_out[(size_t)row * G + g] = only;
+  while (todo) {
+    const int src_lane = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int tg = __shfl_sync(0xffffffffu, g, src_lane);
+    const int trow = __shfl_sync(0xffffffffu, row, src_lane);
+    const size_t trec0 = __shfl_sync(0xffffffffu, (unsigned long long)rec0, src_lane);
+    const float tthr = __shfl_sync(0xffffffffu, thr, src_lane);
+    const bool tover = __shfl_sync(0xffffffffu, (int)overflow, src_lane) != 0;
+    const int src = rows ? rows[trow] : trow;
+    const float* xr = x + (size_t)src * ldx + (size_t)tg * gd;
     double pp = 0.0;
     for (int e = lane; e < gd; e += 32) pp = fma((double)__ldg(xr + e), (double)__ldg(xr + e), pp);
     pp = warp_sum_d(pp);
-    const float* cents = cb.centroids + (size_t)g * K * gd;
-    const double* cc = cb.c_sq64 + (size_t)g * K;
+    const float* cents = cb.centroids + (size_t)tg * K * gd;
+    const double* cc = cb.c_sq64 + (size_t)tg * K;
     double bd = INFINITY;
     int bi = -1;
-    if (overflow) {
+    if (tover) {
       for (int k = 0; k < K; ++k) {
         const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
         if (d < bd) {
@@ -277,11 +305,11 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
     } else {
       // candidates arrive in increasing code order (chunks ascending, columns ascending)
       for (int c = 0; c < nchunk; ++c) {
-        if (w.rec_best[rec0 + c] > thr) continue;
-        const int m = w.rec_cnt[rec0 + c];
+        if (w.rec_best[trec0 + c] > tthr) continue;
+        const int m = w.rec_cnt[trec0 + c];
         for (int i = 0; i < m; ++i) {
-          if (w.rec_score[(rec0 + c) * kVqCap + i] > thr) continue;
-          const int k = w.rec_idx[(rec0 + c) * kVqCap + i];
+          if (w.rec_score[(trec0 + c) * kVqCap + i] > tthr) continue;
+          const int k = w.rec_idx[(trec0 + c) * kVqCap + i];
           const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
           if (d < bd || (d == bd && k < bi)) {
             bd = d;
@@ -290,15 +318,12 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
         }
       }
     }
-    result = bi;
-    if (stats && lane == 0) {
-      atomicAdd(&stats[overflow ? 1 : 0], 1);
+    if (lane == src_lane) {
+      idx_out[(size_t)trow * G + tg] = bi;
+      if (stats) atomicAdd(&stats[tover ? 1 : 0], 1);
     }
   }
-  if (lane == 0) {
-    idx_out[(size_t)row * G + g] = result;
-    if (stats) atomicAdd(&stats[2], n);
-  }
+  if (stats && active) atomicAdd(&stats[2], n);
 }
 
 // ------------------------------------------------------------ decode
@@ -387,6 +412,50 @@ extern "C" int64_t astra_vq_encode_workspace(int M, int groups, int size, int pa
   return (int64_t)carve(nullptr, nullptr, M, groups, size, padded_dim);
 }
 
+// Distance GEMM + windowed-argmin epilogue over `Mg` operand rows (per group), then the
+// finalize over the M tokens.  rec_by_row: records are indexed by source row (pre-split
+// operands cover the whole stack) instead of by token.
+static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const void* a_lo, int lda,
+                            int Mg, VqWorkspace w, const float* x, int M, int ldx,
+                            const int32_t* rows, int rec_by_row, int32_t* idx_out, int32_t* stats,
+                            cudaStream_t s) {
+  const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
+  const int ntile = (K + kVqBN - 1) / kVqBN;
+  const int nchunk = 2 * ntile;
+  CUtensorMap ta, talo, tb, tblo;
+  int st;
+  if ((st = make_tmap_2d(&ta, a_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * Mg, gdp,
+                         lda, kBM, kBK, true)))
+    return st;
+  if ((st = make_tmap_2d(&talo, a_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * Mg, gdp,
+                         lda, kBM, kBK, true)))
+    return st;
+  if ((st = make_tmap_2d(&tb, cb.c_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
+                         gdp, kVqBN, kBK, true)))
+    return st;
+  if ((st = make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
+                         gdp, kVqBN, kBK, true)))
+    return st;
+  VqEpilogue epi{Mg, K, nchunk, cb.c_sq, cb.c_norm_max, w};
+  auto kern = tc_gemm_kernel<kVqBN, 3, 2, VqEpilogue>;
+  constexpr int smem = gemm_smem_bytes<kVqBN, 3, 2>();
+  static bool configured = false;
+  if (!configured) {
+    ASTRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  TileSched sched{(Mg + kBM - 1) / kBM, ntile, G};
+  const int tiles = sched.num_m * sched.num_n * sched.num_b;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, kGemmThreads, smem, s>>>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  const int items = G * M;
+  vq_finalize_kernel<<<(items + 127) / 128, 128, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
+                                                         stats, Mg, rec_by_row);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
 extern "C" int astra_vq_encode(const AstraCodebook* cbp, const float* x, int M, int ldx,
                                const int32_t* rows, int32_t* idx_out, int32_t* stats,
                                void* workspace, int64_t workspace_bytes, void* stream) {
@@ -402,44 +471,37 @@ extern "C" int astra_vq_encode(const AstraCodebook* cbp, const float* x, int M, 
   VqWorkspace w;
   carve(&w, workspace, M, G, K, gdp);
   cudaStream_t s = as_stream(stream);
-  const int nchunk = (K + kVqBN - 1) / kVqBN;
-
   vq_split_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, M, ldx, rows, G, cb.group_dim, gdp, w);
   ASTRA_CUDA_CHECK(cudaGetLastError());
+  return vq_gemm_finalize(cb, w.x_hi, w.x_lo, gdp, M, w, x, M, ldx, rows, 0, idx_out, stats, s);
+}
 
-  CUtensorMap ta, talo, tb, tblo;
-  int st;
-  if ((st = make_tmap_2d(&ta, w.x_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * M, gdp,
-                         gdp, kBM, kBK, true)))
-    return st;
-  if ((st = make_tmap_2d(&talo, w.x_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * M, gdp,
-                         gdp, kBM, kBK, true)))
-    return st;
-  if ((st = make_tmap_2d(&tb, cb.c_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
-                         gdp, kVqBN, kBK, true)))
-    return st;
-  if ((st = make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
-                         gdp, kVqBN, kBK, true)))
-    return st;
-  VqEpilogue epi{M, K, nchunk, cb.c_sq, cb.c_norm_max, w};
-  auto kern = tc_gemm_kernel<kVqBN, 3, 2, VqEpilogue>;
-  constexpr int smem = gemm_smem_bytes<kVqBN, 3, 2>();
-  static bool configured = false;
-  if (!configured) {
-    ASTRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
-  TileSched sched{(M + kBM - 1) / kBM, nchunk, G};
-  const int tiles = sched.num_m * sched.num_n * sched.num_b;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kGemmThreads, smem, s>>>(ta, talo, tb, tblo, gdp, sched, M, K, epi);
-  ASTRA_CUDA_CHECK(cudaGetLastError());
+extern "C" int64_t astra_vq_encode_split_workspace(int R, int size) {
+  return (int64_t)carve(nullptr, nullptr, R, 1, size, 0);
+}
 
-  const int items = G * M;
-  vq_finalize_kernel<<<(items + 7) / 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
-                                                      stats);
-  ASTRA_CUDA_CHECK(cudaGetLastError());
-  return ASTRA_OK;
+extern "C" int astra_vq_encode_split(const AstraCodebook* cbp, const float* x, int ldx,
+                                     const void* x_hi, const void* x_lo, int ld_split,
+                                     const float* x_norm, int R, const int32_t* rows, int M,
+                                     int32_t* idx_out, int32_t* stats, void* workspace,
+                                     int64_t workspace_bytes, void* stream) {
+  ASTRA_REQUIRE(cbp && x && x_hi && x_lo && x_norm && rows && idx_out, ASTRA_ERR_SHAPE,
+                "astra_vq_encode_split: null argument");
+  const AstraCodebook cb = *cbp;
+  ASTRA_REQUIRE(cb.groups == 1 && cb.padded_dim == cb.group_dim, ASTRA_ERR_SHAPE,
+                "astra_vq_encode_split: needs G = 1 and D %% 64 == 0");
+  if (M == 0) return ASTRA_OK;
+  const size_t need = carve(nullptr, nullptr, R, 1, cb.size, 0);
+  ASTRA_REQUIRE((size_t)workspace_bytes >= need, ASTRA_ERR_SHAPE,
+                "astra_vq_encode_split: workspace %lld < %zu bytes", (long long)workspace_bytes,
+                need);
+  VqWorkspace w;
+  carve(&w, workspace, R, 1, cb.size, 0);
+  w.x_hi = nullptr;
+  w.x_lo = nullptr;
+  w.x_norm = const_cast<float*>(x_norm);
+  return vq_gemm_finalize(cb, x_hi, x_lo, ld_split, R, w, x, M, ldx, rows, 1, idx_out, stats,
+                          as_stream(stream));
 }
 
 extern "C" int astra_vq_decode(const AstraCodebook* cbp, const int32_t* idx, int M, float* out,

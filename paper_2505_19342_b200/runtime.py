@@ -25,6 +25,7 @@ _device_layer_compute (cluster.py:176-221) per device and layer.  Design:
 from __future__ import annotations
 
 import contextlib
+import ctypes
 import math
 
 import numpy as np
@@ -97,6 +98,9 @@ class AstraRuntime:
         self._upload(params)
         self._alloc()
         self.graph = None
+        self.graphs = []
+        self.x_slots = [self.x_in]
+        self._slot = 0
         self.trace = None   # test hook: list collecting idx_all per layer
         self.profile = None  # bench hook: {op name: [(start_event, end_event), ...]}
 
@@ -235,8 +239,17 @@ class AstraRuntime:
         self.key_src = e(self.n_keys, dt=torch.int32)
         self.key_src.copy_(self.key_map)
         cb0 = self.layers[0]["cb"]
-        self.vq_ws = e(max(cb0.workspace_bytes(max(self.n_content, 1)) if cb0 else 1, 1),
-                       dt=torch.uint8)
+        # G = 1 and D a multiple of 128: LN1 also emits the bf16 split + row norms of the raw
+        # stack, and the VQ distance GEMM consumes them directly (no separate split pass).
+        self.presplit = (cb0 is not None and self.G == 1 and D in (512, 768, 1024))
+        if self.presplit:
+            self.xs_hi, self.xs_lo = e(R, D, dt=BF16), e(R, D, dt=BF16)
+            self.xnorm = e(R)
+            ws = int(_native.load().astra_vq_encode_split_workspace(R, self.K))
+        else:
+            self.xs_hi = self.xs_lo = self.xnorm = None
+            ws = cb0.workspace_bytes(max(self.n_content, 1)) if cb0 else 1
+        self.vq_ws = e(max(ws, 1), dt=torch.uint8)
         self.vq_stats = torch.zeros(4, dtype=torch.int32, device=dev)
         if self.comm is not None:
             wmax = (B * max(self.sizes) * self.G * self.bits + 31) // 32
@@ -292,11 +305,29 @@ class AstraRuntime:
         cb = lay["cb"]
         if self.capture_inputs is not None:
             self.capture_inputs.append(self.X[self.content_rows.long()].clone())
-        # 1. VQ encode of this GPU's content tokens (cluster.py:272-275)
-        if cb is not None and (self.has_remote or self.encode_at_one_device):
+        encode = cb is not None and (self.has_remote or self.encode_at_one_device)
+        # 1. LN1 over the local stack (content + replica); with pre-split VQ it also writes the
+        #    bf16 hi/lo split and norms of the raw rows from the same read
+        split = self.presplit and encode
+        with self._op("ln1"):
+            _native.call("astra_layernorm_ex", self.X.data_ptr(), R, D, D,
+                         lay["ln1_g"].data_ptr(), lay["ln1_b"].data_ptr(), LN_EPS, None, 0,
+                         self.ln_hi.data_ptr(), _p(self.ln_lo), D,
+                         _p(self.xs_hi) if split else None, _p(self.xs_lo) if split else None, D,
+                         _p(self.xnorm) if split else None, s)
+        # 2. VQ encode of this GPU's content tokens (cluster.py:272-275)
+        if encode:
             with self._op("vq_encode"):
-                cb.encode(self.X, out=self.idx_local, rows=self.content_rows,
-                          workspace=self.vq_ws, stats=self.vq_stats)
+                if split:
+                    _native.call("astra_vq_encode_split", ctypes.byref(cb.struct),
+                                 self.X.data_ptr(), D, self.xs_hi.data_ptr(),
+                                 self.xs_lo.data_ptr(), D, self.xnorm.data_ptr(), R,
+                                 self.content_rows.data_ptr(), self.n_content,
+                                 self.idx_local.data_ptr(), self.vq_stats.data_ptr(),
+                                 self.vq_ws.data_ptr(), self.vq_ws.numel(), s)
+                else:
+                    cb.encode(self.X, out=self.idx_local, rows=self.content_rows,
+                              workspace=self.vq_ws, stats=self.vq_stats)
         # 2. exchange + remote K/V view
         if self.has_remote:
             with self._op("exchange"):
@@ -313,11 +344,6 @@ class AstraRuntime:
             remote = self.qkv
         if self.trace is not None:
             self.trace.append(self.idx_all.clone())
-        # 3. LN1 over the local stack (content + replica)
-        with self._op("ln1"):
-            _native.call("astra_layernorm", self.X.data_ptr(), R, D, D, lay["ln1_g"].data_ptr(),
-                     lay["ln1_b"].data_ptr(), LN_EPS, None, 0, self.ln_hi.data_ptr(),
-                     _p(self.ln_lo), D, s)
         # 4. fused Q|K|V projection
         whi, wlo = lay["wqkv"]
         with self._op("gemm_qkv"):
@@ -353,7 +379,8 @@ class AstraRuntime:
                          residual=self.Hres, out_f32=self.X)
 
     def _embed(self):
-        _native.call("astra_embed_stack", self.x_in.data_ptr(), self.pos.data_ptr(),
+        x_in = self.x_slots[self._slot]
+        _native.call("astra_embed_stack", x_in.data_ptr(), self.pos.data_ptr(),
                      _p(self.cls), self.row_src.data_ptr(), self.row_pos.data_ptr(), self.R,
                      self.D, self.X.data_ptr(), _stream())
 
@@ -400,23 +427,85 @@ class AstraRuntime:
         return self.logits
 
     # -------------------------------------------------------------- CUDA graph
-    def capture(self, warmup: int = 1):
-        """Record ``forward`` (fixed buffers, fixed launch sequence) into a CUDA graph."""
+    def capture(self, warmup: int = 1, slots: int = 1):
+        """Record ``forward`` (fixed buffers, fixed launch sequence) into CUDA graphs, one per
+        input slot (two slots let the next batch's host->device copy overlap this forward)."""
+        while len(self.x_slots) < slots:
+            self.x_slots.append(torch.empty_like(self.x_in))
         for _ in range(warmup):
             self.forward()
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.forward()
-        self.graph = g
-        return g
+        self.graphs = []
+        for slot in range(len(self.x_slots)):
+            self._slot = slot
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.forward()
+            self.graphs.append(g)
+        self._slot = 0
+        self.graph = self.graphs[0]
+        return self.graph
 
-    def run(self):
+    def run(self, slot: int = 0):
         if self.graph is not None:
-            self.graph.replay()
+            self.graphs[slot].replay()
         else:
+            self._slot = slot
             self.forward()
+            self._slot = 0
         return self.logits
+
+    def classify_stream(self, batches, out=None):
+        """Serve a sequence of host batches ([B, T, D] fp32, pinned for async copies).
+
+        Double-buffered: the host->device copy of batch i+1 runs on a copy stream while
+        batch i's forward runs; every batch's logits are copied back and synchronised
+        before the next result is produced.  Returns the list of host logits tensors."""
+        if len(self.x_slots) < 2:
+            try:
+                self.capture(slots=2)
+            except RuntimeError:   # e.g. a collective that cannot be graph-captured: eager
+                torch.cuda.synchronize()
+                self.graph, self.graphs = None, []
+                while len(self.x_slots) < 2:
+                    self.x_slots.append(torch.empty_like(self.x_in))
+        main = torch.cuda.current_stream()
+        copy = getattr(self, "_copy_stream", None) or torch.cuda.Stream(device=self.device)
+        self._copy_stream = copy
+        copied = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        results = []
+        n = len(batches)
+        start, stop = ((0, self.T) if self.comm is None else self.plan.ranges[self.comm.rank])
+
+        def h2d(i):
+            slot = i % 2
+            with torch.cuda.stream(copy):
+                if i >= 2:
+                    copy.wait_event(done[slot])
+                xv = self.x_slots[slot].view(self.B, self.T, self.D)
+                src = batches[i]
+                if self.comm is None:
+                    xv.copy_(src, non_blocking=True)
+                else:  # only this rank's token shard crosses PCIe
+                    xv[:, start:stop].copy_(src, non_blocking=True)
+                copied[slot].record(copy)
+
+        if n:
+            h2d(0)
+        for i in range(n):
+            slot = i % 2
+            main.wait_event(copied[slot])
+            self.run(slot)
+            done[slot].record(main)
+            if i + 1 < n:
+                h2d(i + 1)
+            host = out[i] if out is not None else torch.empty(self.logits.shape, dtype=torch.float32,
+                                                              pin_memory=True)
+            host.copy_(self.logits, non_blocking=True)
+            main.synchronize()   # the batch's result is on the host
+            results.append(host)
+        return results
 
     # ------------------------------------------------------------------ host API
     def stage_input(self, xs):

@@ -21,4 +21,9 @@ for M, N, K in shapes:
     t1 = bench(lambda: kernels.gemm(a, b, out_hi=outh))
     t3 = bench(lambda: kernels.gemm(a, b, a_lo=al, b_lo=bl, out_f32=out))
     tc = bench(lambda: torch.matmul(a, b.T))
+    bias = torch.randn(N, device="cuda")
+    tg = bench(lambda: kernels.gemm(a, b, bias=bias, gelu=True, out_hi=outh))
+    res = torch.randn(M, N, device="cuda")
+    tr = bench(lambda: kernels.gemm(a, b, bias=bias, residual=res, out_f32=out))
+    print(f"   +bias+gelu->bf16 {tg*1e6:.1f}us | +bias+residual->f32 {tr*1e6:.1f}us", flush=True)
     print(f"{M}x{N}x{K}: bf16 {t1*1e6:.1f}us {fl/t1/1e12:.0f} TF/s | bf16x3 {t3*1e6:.1f}us {3*fl/t3/1e12:.0f} TF/s(eff x3) | cublas {tc*1e6:.1f}us {fl/tc/1e12:.0f} TF/s", flush=True)
