@@ -156,6 +156,27 @@ int astra_gather_rows(const float* src, int lds, const int32_t* idx, int rows, i
 int astra_key_map(const int32_t* key_map, int n, const int32_t* codes, int32_t* key_src,
                   void* stream);
 
+/* ------------------------------------------------------ greedy decoding
+ * Generation on the device holding the last prompt token (cluster.py:297-308,
+ * DecodeState/_decode_one model.py:324-358).  All byte-addressed (any dtype).
+ *   gather_kv : cache row (i / n_per) * ld_blocks + i % n_per = [K | V] of key i
+ *               picked through key_src (the decoding device's mixed K/V view)
+ *   append_kv : cache row b * ld_blocks + pos[b] = [K | V] of the new token b
+ *   argmax_rows: out[row * out_stride + (step_pos ? step_pos[row] - pos_base : 0)] =
+ *               argmax (lowest index on ties); next_tok[row] too (nullable)
+ *   decode_advance: pos[b] += 1; segs[b].qpos0 += 1; segs[b].nk += 1 */
+int astra_gather_kv(const int32_t* key_src, int n, int n_per, int ld_blocks, const void* k_local,
+                    const void* v_local, int ld_local_bytes, const void* k_remote,
+                    const void* v_remote, int ld_remote_bytes, int row_bytes, void* cache,
+                    int ld_cache_bytes, void* stream);
+int astra_append_kv(const void* k_new, const void* v_new, int ld_new_bytes, int rows,
+                    const int32_t* pos, int ld_blocks, int row_bytes, void* cache,
+                    int ld_cache_bytes, void* stream);
+int astra_argmax_rows(const float* logits, int rows, int cols, int ld, int32_t* out,
+                      int out_stride, const int32_t* step_pos, int pos_base, int32_t* next_tok,
+                      void* stream);
+int astra_decode_advance(int32_t* pos, int32_t* segs, int rows, void* stream);
+
 /* --------------------------------------------------- mixed-precision attention
  * attention.multihead_attention + tensor.masked_softmax (attention.py:50-73,
  * tensor.py:295-315) over each device's mixed key set (cluster.py:201-212).

@@ -48,6 +48,11 @@ SIGNATURES: dict[str, list] = {
                         _c_int, _c_int, _c_int, _c_int, _c_int, ctypes.c_float, _vp, _vp, _vp,
                         _c_int, _vp],
     "astra_attention_force_simt": [_c_int],
+    "astra_gather_kv": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _c_int,
+                        _vp, _c_int, _vp],
+    "astra_append_kv": [_vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp],
+    "astra_argmax_rows": [_vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _c_int, _vp, _vp],
+    "astra_decode_advance": [_vp, _vp, _c_int, _vp],
     "astra_attention_masked": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
                                _vp],
 }

@@ -179,6 +179,109 @@ __global__ void key_map_kernel(const int32_t* __restrict__ key_map, int n,
   key_src[j] = (m >= 0 || codes == nullptr) ? m : -(codes[-(m + 1)] + 1);
 }
 
+// ---------------------------------------------------------- decode support
+// (greedy generation on the device holding the last prompt token: cluster.py:297-308,
+//  DecodeState / _decode_one model.py:324-358)
+
+// 16-byte vector copy of `bytes` (multiple of 16) by one warp
+__device__ __forceinline__ void warp_copy16(void* dst, const void* src, int bytes, int lane) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  for (int i = lane; i < bytes / 16; i += 32) d[i] = __ldg(s + i);
+}
+
+// cache row (i / n_per) * ld_blocks + i % n_per  <-  [K | V] of key i, gathered via key_src
+__global__ void gather_kv_kernel(const int32_t* __restrict__ key_src, int n, int n_per,
+                                 int ld_blocks, const uint8_t* __restrict__ k_local,
+                                 const uint8_t* __restrict__ v_local, int ld_local,
+                                 const uint8_t* __restrict__ k_remote,
+                                 const uint8_t* __restrict__ v_remote, int ld_remote,
+                                 int row_bytes, uint8_t* __restrict__ cache, int ld_cache) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < n; i += gridDim.x * warps) {
+    const int src = key_src[i];
+    const uint8_t *kp, *vp;
+    if (src >= 0) {
+      kp = k_local + (size_t)src * ld_local;
+      vp = v_local + (size_t)src * ld_local;
+    } else {
+      kp = k_remote + (size_t)(-(src + 1)) * ld_remote;
+      vp = v_remote + (size_t)(-(src + 1)) * ld_remote;
+    }
+    uint8_t* dst = cache + ((size_t)(i / n_per) * ld_blocks + i % n_per) * ld_cache;
+    warp_copy16(dst, kp, row_bytes, lane);
+    warp_copy16(dst + row_bytes, vp, row_bytes, lane);
+  }
+}
+
+// append the new token's K|V (row b of the projection buffer) at cache row b*ld_blocks + pos[b]
+__global__ void append_kv_kernel(const uint8_t* __restrict__ k_new, const uint8_t* __restrict__ v_new,
+                                 int ld_new, int rows, const int32_t* __restrict__ pos,
+                                 int ld_blocks, int row_bytes, uint8_t* __restrict__ cache,
+                                 int ld_cache) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= rows) return;
+  uint8_t* dst = cache + ((size_t)b * ld_blocks + pos[b]) * ld_cache;
+  warp_copy16(dst, k_new + (size_t)b * ld_new, row_bytes, lane);
+  warp_copy16(dst + row_bytes, v_new + (size_t)b * ld_new, row_bytes, lane);
+}
+
+// greedy argmax per row, lowest index on ties (np.argmax, model.py:358 / cluster.py:302)
+__global__ void argmax_rows_kernel(const float* __restrict__ logits, int cols, int ld,
+                                   int32_t* __restrict__ out, int out_stride,
+                                   const int32_t* __restrict__ step_pos, int pos_base,
+                                   int32_t* __restrict__ next_tok) {
+  const int row = blockIdx.x;
+  const float* lr = logits + (size_t)row * ld;
+  float bv = -INFINITY;
+  int bi = 0x7FFFFFFF;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float v = lr[c];
+    if (v > bv) {  // strictly greater: the first (lowest) index of a tie stays
+      bv = v;
+      bi = c;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > bv || (ov == bv && oi < bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[w] = bv;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+      if (sv[i] > bv || (sv[i] == bv && si[i] < bi)) {
+        bv = sv[i];
+        bi = si[i];
+      }
+    const int slot = step_pos ? step_pos[row] - pos_base : 0;
+    out[(size_t)row * out_stride + slot] = bi;
+    if (next_tok) next_tok[row] = bi;
+  }
+}
+
+// one decode step done: every image's position and key count advance by one
+__global__ void decode_advance_kernel(int32_t* __restrict__ pos, int32_t* __restrict__ segs,
+                                      int rows) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= rows) return;
+  pos[b] += 1;
+  segs[b * 6 + 2] += 1;  // query position
+  segs[b * 6 + 5] += 1;  // key count
+}
+
 static int grid_rows(int rows, int warps_per_block) {
   int g = (rows + warps_per_block - 1) / warps_per_block;
   const int cap = num_sms() * 8;
@@ -269,6 +372,49 @@ extern "C" int astra_key_map(const int32_t* key_map, int n, const int32_t* codes
                              int32_t* key_src, void* stream) {
   if (n == 0) return ASTRA_OK;
   key_map_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(key_map, n, codes, key_src);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_gather_kv(const int32_t* key_src, int n, int n_per, int ld_blocks,
+                               const void* k_local, const void* v_local, int ld_local_bytes,
+                               const void* k_remote, const void* v_remote, int ld_remote_bytes,
+                               int row_bytes, void* cache, int ld_cache_bytes, void* stream) {
+  ASTRA_REQUIRE(row_bytes % 16 == 0 && n_per > 0, ASTRA_ERR_SHAPE, "gather_kv: bad row size");
+  if (n == 0) return ASTRA_OK;
+  gather_kv_kernel<<<grid_rows(n, 8), 256, 0, as_stream(stream)>>>(
+      key_src, n, n_per, ld_blocks, (const uint8_t*)k_local, (const uint8_t*)v_local,
+      ld_local_bytes, (const uint8_t*)k_remote, (const uint8_t*)v_remote, ld_remote_bytes,
+      row_bytes, (uint8_t*)cache, ld_cache_bytes);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_append_kv(const void* k_new, const void* v_new, int ld_new_bytes, int rows,
+                               const int32_t* pos, int ld_blocks, int row_bytes, void* cache,
+                               int ld_cache_bytes, void* stream) {
+  ASTRA_REQUIRE(row_bytes % 16 == 0, ASTRA_ERR_SHAPE, "append_kv: bad row size");
+  if (rows == 0) return ASTRA_OK;
+  append_kv_kernel<<<(rows + 7) / 8, 256, 0, as_stream(stream)>>>(
+      (const uint8_t*)k_new, (const uint8_t*)v_new, ld_new_bytes, rows, pos, ld_blocks, row_bytes,
+      (uint8_t*)cache, ld_cache_bytes);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_argmax_rows(const float* logits, int rows, int cols, int ld, int32_t* out,
+                                 int out_stride, const int32_t* step_pos, int pos_base,
+                                 int32_t* next_tok, void* stream) {
+  if (rows == 0) return ASTRA_OK;
+  argmax_rows_kernel<<<rows, 1024, 0, as_stream(stream)>>>(logits, cols, ld, out, out_stride,
+                                                            step_pos, pos_base, next_tok);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_decode_advance(int32_t* pos, int32_t* segs, int rows, void* stream) {
+  if (rows == 0) return ASTRA_OK;
+  decode_advance_kernel<<<(rows + 127) / 128, 128, 0, as_stream(stream)>>>(pos, segs, rows);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }

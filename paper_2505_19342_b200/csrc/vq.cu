@@ -237,64 +237,58 @@ __device__ __forceinline__ double exact_d2(const float* xr, const float* c, int 
   return (pp - 2.0 * pc) + cc;
 }
 
-// One thread decides one (g, row): the window candidates of its 2*ceil(K/256) chunk records
-// are merged; a single survivor is the answer.  Rows with several survivors (or a chunk whose
-// candidate list overflowed) are then re-ranked one after another by the whole warp in exact
-// fp64 — the reference's own expression (||p||^2 - 2 p.c) + ||c||^2, ties to the lowest index.
+// One warp per (g, row).  Lane c reads chunk record c (2*ceil(K/256) records per row); the
+// window test, survivor count and the single survivor come out of warp shuffles.  A single
+// survivor is the answer; several (or a chunk whose candidate list overflowed) are re-ranked
+// by the warp in exact fp64 with the reference's expression (||p||^2 - 2 p.c) + ||c||^2,
+// ties to the lowest index.
 __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x, int M, int ldx,
                                    const int32_t* __restrict__ rows, VqWorkspace w, int nchunk,
                                    int32_t* __restrict__ idx_out, int32_t* __restrict__ stats,
                                    int Mrec, int rec_by_row) {
-  const int G = cb.groups, K = cb.size, gd = cb.group_dim;
-  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  const int warps = blockDim.x >> 5;
+  const int item = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  const bool active = item < G * M;
-  int g = 0, row = 0, rr = 0, n = 0, only = -1;
-  bool overflow = false;
-  float thr = 0.f;
-  size_t rec0 = 0;
-  if (active) {
-    g = item / M;
-    row = item % M;
-    // records / norms are indexed by token (gathered split) or by source row (pre-split stack)
-    rr = rec_by_row ? rows[row] : row;
-    rec0 = ((size_t)g * Mrec + rr) * nchunk;
-    float best = INFINITY;
-    for (int c = 0; c < nchunk; ++c) best = fminf(best, w.rec_best[rec0 + c]);
-    thr = best + 2.0f * score_delta(w.x_norm[(size_t)g * Mrec + rr], cb.c_norm_max[g]);
-    for (int c = 0; c < nchunk; ++c) {
-      if (w.rec_best[rec0 + c] > thr) continue;
-      const int cnt = w.rec_cnt[rec0 + c];
-      if (cnt > kVqCap) overflow = true;
-      const int m = cnt < kVqCap ? cnt : kVqCap;
-      for (int i = 0; i < m; ++i)
-        if (w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
-          ++n;
-          only = w.rec_idx[(rec0 + c) * kVqCap + i];
-        }
-    }
+  const int G = cb.groups, K = cb.size, gd = cb.group_dim;
+  if (item >= G * M) return;
+  const int g = item / M, row = item % M;
+  // records / norms are indexed by token (gathered split) or by source row (pre-split stack)
+  const int rr = rec_by_row ? rows[row] : row;
+  const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
+  float best = INFINITY;
+  for (int c = lane; c < nchunk; c += 32) best = fminf(best, w.rec_best[rec0 + c]);
+  for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  const float thr = best + 2.0f * score_delta(w.x_norm[(size_t)g * Mrec + rr], cb.c_norm_max[g]);
+  int n = 0, only = 0x7FFFFFFF;
+  int overflow = 0;
+  for (int c = lane; c < nchunk; c += 32) {
+    if (w.rec_best[rec0 + c] > thr) continue;
+    const int cnt = w.rec_cnt[rec0 + c];
+    if (cnt > kVqCap) overflow = 1;
+    const int m = cnt < kVqCap ? cnt : kVqCap;
+    for (int i = 0; i < m; ++i)
+      if (w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
+        ++n;
+        only = min(only, w.rec_idx[(rec0 + c) * kVqCap + i]);
+      }
   }
-  const bool need = active && (overflow || n > 1);
-  unsigned todo = __ballot_sync(0xffffffffu, need);
-  if (active && !need) idx_out[(size_t)row * G + g] = only;
-  while (todo) {
-    const int src_lane = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const int tg = __shfl_sync(0xffffffffu, g, src_lane);
-    const int trow = __shfl_sync(0xffffffffu, row, src_lane);
-    const size_t trec0 = __shfl_sync(0xffffffffu, (unsigned long long)rec0, src_lane);
-    const float tthr = __shfl_sync(0xffffffffu, thr, src_lane);
-    const bool tover = __shfl_sync(0xffffffffu, (int)overflow, src_lane) != 0;
-    const int src = rows ? rows[trow] : trow;
-    const float* xr = x + (size_t)src * ldx + (size_t)tg * gd;
+  for (int o = 16; o; o >>= 1) {
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+    only = min(only, __shfl_xor_sync(0xffffffffu, only, o));
+    overflow |= __shfl_xor_sync(0xffffffffu, overflow, o);
+  }
+  int result = only;
+  if (overflow || n > 1) {
+    const int src = rows ? rows[row] : row;
+    const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
     double pp = 0.0;
     for (int e = lane; e < gd; e += 32) pp = fma((double)__ldg(xr + e), (double)__ldg(xr + e), pp);
     pp = warp_sum_d(pp);
-    const float* cents = cb.centroids + (size_t)tg * K * gd;
-    const double* cc = cb.c_sq64 + (size_t)tg * K;
+    const float* cents = cb.centroids + (size_t)g * K * gd;
+    const double* cc = cb.c_sq64 + (size_t)g * K;
     double bd = INFINITY;
     int bi = -1;
-    if (tover) {
+    if (overflow) {
       for (int k = 0; k < K; ++k) {
         const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
         if (d < bd) {
@@ -303,13 +297,13 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
         }
       }
     } else {
-      // candidates arrive in increasing code order (chunks ascending, columns ascending)
+      // candidates in increasing code order (chunks ascending, columns ascending)
       for (int c = 0; c < nchunk; ++c) {
-        if (w.rec_best[trec0 + c] > tthr) continue;
-        const int m = w.rec_cnt[trec0 + c];
+        if (w.rec_best[rec0 + c] > thr) continue;
+        const int m = w.rec_cnt[rec0 + c];
         for (int i = 0; i < m; ++i) {
-          if (w.rec_score[(trec0 + c) * kVqCap + i] > tthr) continue;
-          const int k = w.rec_idx[(trec0 + c) * kVqCap + i];
+          if (w.rec_score[(rec0 + c) * kVqCap + i] > thr) continue;
+          const int k = w.rec_idx[(rec0 + c) * kVqCap + i];
           const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
           if (d < bd || (d == bd && k < bi)) {
             bd = d;
@@ -318,12 +312,13 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
         }
       }
     }
-    if (lane == src_lane) {
-      idx_out[(size_t)trow * G + tg] = bi;
-      if (stats) atomicAdd(&stats[tover ? 1 : 0], 1);
-    }
+    result = bi;
+    if (stats && lane == 0) atomicAdd(&stats[overflow ? 1 : 0], 1);
   }
-  if (stats && active) atomicAdd(&stats[2], n);
+  if (lane == 0) {
+    idx_out[(size_t)row * G + g] = result;
+    if (stats) atomicAdd(&stats[2], n);
+  }
 }
 
 // ------------------------------------------------------------ decode
@@ -450,8 +445,8 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
   kern<<<grid, kGemmThreads, smem, s>>>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   const int items = G * M;
-  vq_finalize_kernel<<<(items + 127) / 128, 128, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
-                                                         stats, Mg, rec_by_row);
+  vq_finalize_kernel<<<(items + 7) / 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
+                                                      stats, Mg, rec_by_row);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }

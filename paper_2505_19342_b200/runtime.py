@@ -33,6 +33,7 @@ import torch
 
 from . import _native, kernels
 from .errors import ShapeError
+from .layout import sp_layout
 from .model import LN_EPS, class_owner_ids
 from .vq import DeviceCodebook, index_bits
 
@@ -58,9 +59,24 @@ class TorchDistExchange:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo (CPU tests, or several ranks sharing one GPU) moves host copies
+        self.host_staged = dist.get_backend(group) == "gloo"
 
     def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
-        self.dist.all_gather_into_tensor(out, inp, group=self.group)
+        if not self.host_staged:
+            self.dist.all_gather_into_tensor(out, inp, group=self.group)
+            return
+        parts = [torch.empty_like(inp, device="cpu") for _ in range(self.world)]
+        self.dist.all_gather(parts, inp.cpu(), group=self.group)
+        out.copy_(torch.cat(parts).view_as(out))
+
+    def broadcast(self, t: torch.Tensor, src: int) -> None:
+        if not self.host_staged:
+            self.dist.broadcast(t, src=src, group=self.group)
+            return
+        h = t.cpu()
+        self.dist.broadcast(h, src=src, group=self.group)
+        t.copy_(h)
 
 
 class AstraRuntime:
@@ -106,57 +122,26 @@ class AstraRuntime:
 
     # ------------------------------------------------------------------ layout
     def _build_layout(self):
-        T, B = self.T, self.B
-        sizes = self.plan.shard_sizes()
-        starts = [r[0] for r in self.plan.ranges]
-        owner = self.plan.owner_of()
-        gofs = np.concatenate([[0], np.cumsum([B * s for s in sizes])]).astype(np.int64)
-        rows = 0
-        content, row_src, row_pos, segs, key_map, key_pos, rep_rows = [], [], [], [], [], [], []
-        self.row_base = {}
-        for v in self.local:
-            rep = 1 if v in self.owners else 0
-            for b in range(B):
-                base = rows
-                self.row_base[(v, b)] = base
-                for r in range(sizes[v]):
-                    content.append(base + r)
-                    row_src.append(b * T + starts[v] + r)
-                    row_pos.append(starts[v] + r)
-                if rep:
-                    row_src.append(-1)
-                    row_pos.append(0)
-                    rep_rows.append(base + sizes[v])
-                k0 = len(key_map)
-                for j in range(T):
-                    e = int(owner[j])
-                    if e == v:
-                        key_map.append(base + j - starts[v])
-                    else:
-                        key_map.append(-int(gofs[e] + b * sizes[e] + (j - starts[e]) + 1))
-                    key_pos.append(j)
-                if rep:
-                    key_map.append(base + sizes[v])
-                    key_pos.append(-1)
-                segs.append([base, sizes[v] + rep, starts[v], sizes[v], k0, T + rep])
-                rows += sizes[v] + rep
+        lay = sp_layout(self.T, self.plan.ranges, self.B, self.local, self.owners)
         dev = self.device
-        i32 = lambda a: torch.tensor(np.asarray(a, dtype=np.int32), device=dev)  # noqa: E731
-        self.R = rows
-        self.sizes, self.starts = sizes, starts
-        self.n_content = len(content)
-        self.n_content_all = int(gofs[-1])
-        self.gofs = gofs
-        self.content_rows = i32(content)
-        self.row_src, self.row_pos = i32(row_src), i32(row_pos)
-        self.segs = i32(np.asarray(segs).reshape(-1))
-        self.n_segs = len(segs)
-        self.key_map, self.key_pos = i32(key_map), i32(key_pos)
-        self.n_keys = len(key_map)
-        self.rep_rows = i32(rep_rows) if rep_rows else None
-        self.max_nq = max(s[1] for s in segs)
+        i32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev)  # noqa: E731
+        self.row_base = lay.row_base
+        self.R = lay.rows
+        self.sizes = self.plan.shard_sizes()
+        self.starts = [r[0] for r in self.plan.ranges]
+        self.n_content = len(lay.content_rows)
+        self.n_content_all = int(lay.gofs[-1])
+        self.gofs = lay.gofs
+        self.content_rows = i32(lay.content_rows)
+        self.row_src, self.row_pos = i32(lay.row_src), i32(lay.row_pos)
+        self.segs = i32(lay.segs.reshape(-1))
+        self.n_segs = lay.segs.shape[0]
+        self.key_map, self.key_pos = i32(lay.key_map), i32(lay.key_pos)
+        self.n_keys = len(lay.key_map)
+        self.rep_rows = i32(lay.rep_rows) if len(lay.rep_rows) else None
+        self.max_nq = int(lay.segs[:, 1].max())
         self.has_remote = self.N > 1
-        self.payload_bits = [B * s * self.G * self.bits for s in sizes]
+        self.payload_bits = [self.B * s * self.G * self.bits for s in self.sizes]
 
     # ------------------------------------------------------------------ params
     def _wt(self, w_in_out: np.ndarray):
@@ -265,6 +250,8 @@ class AstraRuntime:
             self.kvhat = e(n, 2 * D, dt=BF16 if self.fast else torch.float32)
             self.dec_err = torch.zeros(1, dtype=torch.int32, device=dev)
         n_rep_local = 0 if self.rep_rows is None else self.rep_rows.numel()
+        if self.mode == "generate":
+            self._alloc_decode()
         if self.mode == "classify":
             self.reps_local = e(max(n_rep_local, 1), D)
             self.reps_all = e(len(self.owners) * B, D) if self.comm is not None else self.reps_local
@@ -272,6 +259,46 @@ class AstraRuntime:
             self.pool_hi = e(B, D, dt=BF16)
             self.pool_lo = None if self.fast else e(B, D, dt=BF16)
             self.logits = e(B, self.classes)
+
+    # ------------------------------------------------------------ decode state
+    def _alloc_decode(self):
+        """Greedy generation on device N-1 (cluster.py:297-308): KV cache per layer holding
+        its mixed view of the prompt (own rows full precision, remote rows K^/V^ of the
+        received codes) plus every generated token, as DecodeState (model.py:324-334)."""
+        dev, B, D, T = self.device, self.B, self.D, self.T
+        self.dec_dev = self.N - 1
+        self.decodes = self.dec_dev in self.local
+        self.maxT = self.cfg.max_tokens
+        i32 = lambda a: torch.tensor(np.asarray(a, dtype=np.int32), device=dev)  # noqa: E731
+        sizes = self.sizes
+        v = self.dec_dev
+        # last content row of device N-1 for every image; its segment key range
+        self.last_rows = i32([self.row_base[(v, b)] + sizes[v] - 1 for b in range(B)]) \
+            if self.decodes else None
+        if self.decodes:
+            seg_idx = self.local.index(v) * B
+            self.dec_k0 = int(self.segs.view(-1, 6)[seg_idx, 4].item())
+        ebytes = 2 if self.fast else 4
+        cdt = BF16 if self.fast else torch.float32
+        self.ebytes = ebytes
+        self.kv_cache = [torch.zeros(B * self.maxT, 2 * D, dtype=cdt, device=dev)
+                         for _ in range(self.L)] if self.decodes else []
+        self.dec_X = torch.empty(B, D, device=dev)
+        self.dec_H = torch.empty(B, D, device=dev)
+        self.dec_ln_hi = torch.empty(B, D, dtype=BF16, device=dev)
+        self.dec_ln_lo = None if self.fast else torch.empty(B, D, dtype=BF16, device=dev)
+        self.dec_qkv = torch.empty(B, 3 * D, dtype=cdt, device=dev)
+        self.dec_o_hi = torch.empty(B, D, dtype=BF16, device=dev)
+        self.dec_o_lo = None if self.fast else torch.empty(B, D, dtype=BF16, device=dev)
+        self.dec_f_hi = torch.empty(B, 4 * D, dtype=BF16, device=dev)
+        self.dec_f_lo = None if self.fast else torch.empty(B, 4 * D, dtype=BF16, device=dev)
+        self.dec_logits = torch.empty(B, self.classes, device=dev)
+        self.next_tok = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.dec_pos = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.dec_segs = torch.zeros(B * 6, dtype=torch.int32, device=dev)
+        self.dec_key_src = i32([b * self.maxT + j for b in range(B) for j in range(self.maxT)])
+        self.dec_key_pos = i32([j for _ in range(B) for j in range(self.maxT)])
+        self.classes_out = None
 
     # ----------------------------------------------------------------- forward
     def _op(self, name: str):
@@ -350,6 +377,15 @@ class AstraRuntime:
             kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo,
                          out_f32=None if self.fast else self.qkv,
                          out_hi=self.qkv if self.fast else None)
+        if self.mode == "generate" and self.decodes:
+            # DecodeState capture (cluster.py:285-288): device N-1's K|V view of the prompt
+            e = self.ebytes
+            with self._op("kv_capture"):
+                _native.call("astra_gather_kv", self.key_src.data_ptr() + 4 * self.dec_k0,
+                             self.B * self.T, self.T, self.maxT, _p(self.qkv, D),
+                             _p(self.qkv, 2 * D), 3 * D * e, _p(remote, 0), _p(remote, D),
+                             remote.stride(0) * e, D * e, self.kv_cache[l].data_ptr(), 2 * D * e,
+                             s)
         # 5. mixed-precision attention
         ld_r = remote.stride(0)
         with self._op("attention"):
@@ -379,7 +415,8 @@ class AstraRuntime:
                          residual=self.Hres, out_f32=self.X)
 
     def _embed(self):
-        x_in = self.x_slots[self._slot]
+        # classify: x + pos (model.py:275-280); generate: embedding[ids] + pos (model.py:283-288)
+        x_in = self.emb if self.mode == "generate" else self.x_slots[self._slot]
         _native.call("astra_embed_stack", x_in.data_ptr(), self.pos.data_ptr(),
                      _p(self.cls), self.row_src.data_ptr(), self.row_pos.data_ptr(), self.R,
                      self.D, self.X.data_ptr(), _stream())
@@ -424,7 +461,8 @@ class AstraRuntime:
         if self.mode == "classify":
             with self._op("tail"):
                 self._classify_tail()
-        return self.logits
+            return self.logits
+        return None
 
     # -------------------------------------------------------------- CUDA graph
     def capture(self, warmup: int = 1, slots: int = 1):
@@ -521,6 +559,87 @@ class AstraRuntime:
             return
         for l in range(self.L):
             ledger.record_exchange(l, self.payload_bits)
+
+    # ---------------------------------------------------------------- generate
+    def _gemm_rows(self, w, a_hi, a_lo, **kw):
+        whi, wlo = w
+        kernels.gemm(a_hi, whi, a_lo=a_lo, b_lo=wlo, **kw)
+
+    def _head_argmax(self, x_rows: torch.Tensor, out: torch.Tensor, steps: int, first: bool):
+        """final LN -> head -> greedy argmax (lowest id on ties, cluster.py:299-302)."""
+        B, D, s = self.B, self.D, _stream()
+        _native.call("astra_layernorm", x_rows.data_ptr(), B, D, D, self.final_g.data_ptr(),
+                     self.final_b.data_ptr(), LN_EPS, None, 0, self.dec_ln_hi.data_ptr(),
+                     _p(self.dec_ln_lo), D, s)
+        self._gemm_rows(self.head, self.dec_ln_hi, self.dec_ln_lo, out_f32=self.dec_logits)
+        _native.call("astra_argmax_rows", self.dec_logits.data_ptr(), B, self.classes,
+                     self.classes, out.data_ptr(), steps, None if first else self.dec_pos.data_ptr(),
+                     self.T - 1, self.next_tok.data_ptr(), s)
+
+    def _decode_step(self, out: torch.Tensor, steps: int):
+        """One greedy step for every image (model.py:337-358) on the decoding device."""
+        B, D, s = self.B, self.D, _stream()
+        e = self.ebytes
+        X, H = self.dec_X, self.dec_H
+        _native.call("astra_embed_stack", self.emb.data_ptr(), self.pos.data_ptr(), None,
+                     self.next_tok.data_ptr(), self.dec_pos.data_ptr(), B, D, X.data_ptr(), s)
+        scale = float(np.float32(1.0 / math.sqrt(self.dk)))
+        for l, lay in enumerate(self.layers):
+            cache = self.kv_cache[l]
+            _native.call("astra_layernorm", X.data_ptr(), B, D, D, lay["ln1_g"].data_ptr(),
+                         lay["ln1_b"].data_ptr(), LN_EPS, None, 0, self.dec_ln_hi.data_ptr(),
+                         _p(self.dec_ln_lo), D, s)
+            self._gemm_rows(lay["wqkv"], self.dec_ln_hi, self.dec_ln_lo,
+                            out_f32=None if self.fast else self.dec_qkv,
+                            out_hi=self.dec_qkv if self.fast else None)
+            _native.call("astra_append_kv", _p(self.dec_qkv, D), _p(self.dec_qkv, 2 * D),
+                         3 * D * e, B, self.dec_pos.data_ptr(), self.maxT, D * e,
+                         cache.data_ptr(), 2 * D * e, s)
+            _native.call("astra_attention", self.dec_qkv.data_ptr(), 3 * D, cache.data_ptr(),
+                         _p(cache, D), 2 * D, cache.data_ptr(), _p(cache, D), 2 * D,
+                         self.dec_key_src.data_ptr(), self.dec_key_pos.data_ptr(),
+                         self.dec_segs.data_ptr(), B, 1, self.H, self.dk, 0, int(self.fast),
+                         scale, None, self.dec_o_hi.data_ptr(), _p(self.dec_o_lo), D, s)
+            self._gemm_rows(lay["wo"], self.dec_o_hi, self.dec_o_lo, residual=X, out_f32=H)
+            _native.call("astra_layernorm", H.data_ptr(), B, D, D, lay["ln2_g"].data_ptr(),
+                         lay["ln2_b"].data_ptr(), LN_EPS, None, 0, self.dec_ln_hi.data_ptr(),
+                         _p(self.dec_ln_lo), D, s)
+            self._gemm_rows(lay["w1"], self.dec_ln_hi, self.dec_ln_lo, bias=lay["b1"], gelu=True,
+                            out_hi=self.dec_f_hi, out_lo=self.dec_f_lo)
+            self._gemm_rows(lay["w2"], self.dec_f_hi, self.dec_f_lo, bias=lay["b2"], residual=H,
+                            out_f32=X)
+        self._head_argmax(X, out, steps, first=False)
+        _native.call("astra_decode_advance", self.dec_pos.data_ptr(), self.dec_segs.data_ptr(), B, s)
+
+    def generate(self, ids, steps: int, ledger=None) -> np.ndarray:
+        """Sequence-parallel causal prefill, then greedy decode on device N-1
+        (cluster.py:243-308).  ids: [B, T] prompt token ids -> [B, steps] generated ids."""
+        if self.mode != "generate":
+            raise ValueError("runtime was not built for generate mode")
+        B, T, dev = self.B, self.T, self.device
+        ids = np.asarray(ids, dtype=np.int64).reshape(B, T)
+        if ids.size and (ids.min() < 0 or ids.max() >= self.emb.shape[0]):
+            raise ShapeError("gather_rows: id out of range")
+        src = np.empty(self.R, dtype=np.int32)
+        for (v, b), base in self.row_base.items():
+            st, n = self.starts[v], self.sizes[v]
+            src[base:base + n] = ids[b, st:st + n]
+        self.row_src.copy_(torch.from_numpy(src))
+        out = torch.zeros(B, max(steps, 1), dtype=torch.int32, device=dev)
+        self.forward()
+        self.record_ledger(ledger)
+        if self.decodes and steps > 0:
+            _native.call("astra_gather_rows", self.X.data_ptr(), self.D, self.last_rows.data_ptr(),
+                         B, self.D, self.dec_X.data_ptr(), self.D, _stream())
+            self._head_argmax(self.dec_X, out, steps, first=True)
+            segs = np.array([[b, 1, T, 1, b * self.maxT, T + 1] for b in range(B)], np.int32)
+            self.dec_segs.copy_(torch.from_numpy(segs.reshape(-1)))
+            self.dec_pos.fill_(T)
+            for _ in range(1, steps):
+                self._decode_step(out, steps)
+        if self.comm is not None:
+            self.comm.broadcast(out, src=self.dec_dev)
+        return out[:, :steps].cpu().numpy()
 
     def classify_numpy(self, xs: np.ndarray, ledger=None) -> np.ndarray:
         self.stage_input(xs)

@@ -68,6 +68,42 @@ def test_classify_parity_vs_reference(cuda, name, n, cls_mode):
     np.testing.assert_array_equal(got, GOLD[f"{tag}_indices"])
 
 
+@pytest.mark.parametrize("n", [1, 2, 4])
+@pytest.mark.parametrize("precision", ["parity", "fast"])
+def test_generate_matches_reference(cuda, n, precision):
+    """Causal SP prefill + greedy decode on device N-1 (cluster.py:243-308): same tokens."""
+    from paper_2505_19342_b200 import cluster
+    params, op, inputs = _setup("gen")
+    m = META["gen"]
+    plan = cluster.partition_tokens(m["tokens"], n, class_replication=False)
+    res = cluster.run_inference(params, plan, inputs, "generate", steps=m["steps"],
+                                precision=precision)
+    tag = f"gen_n{n}"
+    assert res.output == [int(t) for t in GOLD[f"{tag}_output"]]
+    assert res.ledger.to_csv() == META[f"{tag}_ledger"]
+    assert cluster.run_inference(params, plan, inputs, "generate", steps=0).output == []
+
+
+def test_generate_gpt2_width_vs_oracle(cuda):
+    """GPT-2 block width (D=768, H=12) causal prefill over 4 devices + 5 decode steps."""
+    from paper_2505_19342_b200 import cluster, model, vq
+    kw = dict(layers=2, hidden=768, heads=12, vocab_or_classes=300, max_tokens=80, causal=True,
+              codebook_size=64)
+    params = model.init_params(model.ModelConfig(**kw), seed=5)
+    op = O.init_params(O.Config(**kw), seed=5)
+    rng = np.random.default_rng(5)
+    data = [rng.integers(0, 300, size=65) for _ in range(4)]
+    O.initialize_codebooks(op, data, "lm", seed=5, iterations=4)
+    for i, b in enumerate(params.blocks):
+        b.codebook = vq.Codebook(layer_id=i, groups=1, centroids=op.codebooks[i])
+    ids = rng.integers(0, 300, size=64)
+    ranges = O.partition_tokens(64, 4)
+    ref = O.run_inference(op, ranges, ids, "generate", steps=5)
+    plan = cluster.partition_tokens(64, 4, class_replication=False)
+    got = cluster.run_inference(params, plan, ids, "generate", steps=5)
+    assert got.output == ref.output
+
+
 @pytest.mark.parametrize("n", [1, 4])
 def test_classify_fast_mode_tolerance(cuda, n):
     from paper_2505_19342_b200 import cluster
