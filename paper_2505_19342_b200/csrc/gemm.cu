@@ -12,13 +12,14 @@
 
 namespace astra {
 
-// fp32 staging tile [32 rows][32 floats]: 16B chunk c of row r lives at slot c ^ (r & 7)
-__device__ __forceinline__ float4* st_f32(uint8_t* stage, int r, int c) {
-  return reinterpret_cast<float4*>(stage + r * 128 + ((c ^ (r & 7)) << 4));
+// Warp-private staging (kEpiStageBytes): a 32-row x 16-column tile, 64 B (fp32) or 32 B (bf16)
+// per row, with 16-byte chunks XOR-swizzled so the row-per-thread side and the coalesced
+// side are both conflict-free (4 wavefronts per 512 B).
+__device__ __forceinline__ float4* st_f32(uint8_t* stage, int r, int c) {  // c in 0..3
+  return reinterpret_cast<float4*>(stage + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
 }
-// bf16 staging tile [32 rows][32 bf16 = 64 B]: chunk c (0..3) of row r at slot c ^ ((r>>1)&3)
-__device__ __forceinline__ uint4* st_bf(uint8_t* stage, int r, int c) {
-  return reinterpret_cast<uint4*>(stage + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+__device__ __forceinline__ uint4* st_bf(uint8_t* stage, int r, int c) {    // c in 0..1
+  return reinterpret_cast<uint4*>(stage + r * 32 + ((c ^ ((r >> 2) & 1)) << 4));
 }
 
 struct StdEpilogue {
@@ -36,14 +37,14 @@ struct StdEpilogue {
   int vec;  // all row pitches / bases allow 16-byte vectors
 
   __device__ __forceinline__ void store_bf16(uint8_t* stage, __nv_bfloat16* out, int row0,
-                                             int col0, const __nv_bfloat16 (&h)[32]) const {
+                                             int col0, const uint32_t (&h)[8]) const {
     const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) *st_bf(stage, lane, c) = *reinterpret_cast<const uint4*>(h + 8 * c);
+    *st_bf(stage, lane, 0) = make_uint4(h[0], h[1], h[2], h[3]);
+    *st_bf(stage, lane, 1) = make_uint4(h[4], h[5], h[6], h[7]);
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int rr = i * 8 + (lane >> 2), ch = lane & 3, grow = row0 + rr;
+    for (int i = 0; i < 2; ++i) {
+      const int rr = i * 16 + (lane >> 1), ch = lane & 1, grow = row0 + rr;
       if (grow < M)
         *reinterpret_cast<uint4*>(out + (size_t)grow * ld_bf + col0 + ch * 8) = *st_bf(stage, rr, ch);
     }
@@ -51,30 +52,31 @@ struct StdEpilogue {
   }
 
   __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
-                                             int cb, int ce, uint8_t* stage) const {
+                                             int cb, int ce, int /*part*/, uint8_t* stage) const {
     const int lane = threadIdx.x & 31;
     const int row0 = tc.m_blk * kBM + row_in_tile - lane;  // first row of this warp's slab
     const int row = row0 + lane;
     const bool row_ok = row < M;
-    float* sbias = reinterpret_cast<float*>(stage + 4096);
-    for (int c0 = cb; c0 < ce; c0 += 32) {
+    float* sbias = reinterpret_cast<float*>(stage + 2048);
+#pragma unroll 1
+    for (int c0 = cb; c0 < ce; c0 += 16) {
       const int col0 = tc.n_blk * BN + c0;
       // one coalesced bias load per warp, issued before the TMEM load so the latencies overlap
-      const float bl = (bias && col0 + lane < N) ? __ldg(bias + col0 + lane) : 0.f;
-      uint32_t r[32];
-      tmem_ld32(taddr + c0, r);
+      const float bl = (bias && lane < 16 && col0 + lane < N) ? __ldg(bias + col0 + lane) : 0.f;
+      uint32_t r[16];
+      tmem_ld16(taddr + c0, r);
       tmem_ld_wait();
       if (col0 >= N) continue;  // warp-uniform
-      const bool full = (col0 + 32 <= N);
+      const bool full = (col0 + 16 <= N);
       const bool fast = full && vec;
-      float v[32];
+      float v[16];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
       if (bias) {
-        sbias[lane] = bl;
+        if (lane < 16) sbias[lane] = bl;
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
+        for (int j = 0; j < 16; j += 4) {
           const float4 b4 = *reinterpret_cast<const float4*>(sbias + j);  // broadcast read
           v[j] += b4.x;
           v[j + 1] += b4.y;
@@ -85,20 +87,20 @@ struct StdEpilogue {
       }
       if (gelu) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+        for (int j = 0; j < 16; ++j) v[j] = gelu_erf(v[j]);
       }
       if (residual) {
         if (fast) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = i * 4 + (lane >> 3), ch = lane & 7, grow = row0 + rr;
+          for (int i = 0; i < 4; ++i) {
+            const int rr = i * 8 + (lane >> 2), ch = lane & 3, grow = row0 + rr;
             if (grow < M)
               *st_f32(stage, rr, ch) =
                   __ldg(reinterpret_cast<const float4*>(residual + (size_t)grow * ld_res + col0) + ch);
           }
           __syncwarp();
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < 4; ++c) {
             const float4 q = *st_f32(stage, lane, c);
             v[4 * c] = q.x + v[4 * c];
             v[4 * c + 1] = q.y + v[4 * c + 1];
@@ -108,19 +110,19 @@ struct StdEpilogue {
           __syncwarp();
         } else if (row_ok) {
           const float* rp = residual + (size_t)row * ld_res + col0;
-          for (int j = 0; j < 32; ++j)
+          for (int j = 0; j < 16; ++j)
             if (col0 + j < N) v[j] = rp[j] + v[j];
         }
       }
       if (out_f32) {
         if (fast) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
+          for (int c = 0; c < 4; ++c)
             *st_f32(stage, lane, c) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
           __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = i * 4 + (lane >> 3), ch = lane & 7, grow = row0 + rr;
+          for (int i = 0; i < 4; ++i) {
+            const int rr = i * 8 + (lane >> 2), ch = lane & 3, grow = row0 + rr;
             if (grow < M)
               *(reinterpret_cast<float4*>(out_f32 + (size_t)grow * ld_f32 + col0) + ch) =
                   *st_f32(stage, rr, ch);
@@ -128,24 +130,31 @@ struct StdEpilogue {
           __syncwarp();
         } else if (row_ok) {
           float* op = out_f32 + (size_t)row * ld_f32 + col0;
-          for (int j = 0; j < 32; ++j)
+          for (int j = 0; j < 16; ++j)
             if (col0 + j < N) op[j] = v[j];
         }
       }
       if (out_hi) {
-        __nv_bfloat16 hi[32], lo[32];
+        uint32_t hp[8], lp[8];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) split_bf16(v[j], hi[j], lo[j]);
+        for (int j = 0; j < 16; j += 2) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j], v[j + 1]);
+          __nv_bfloat162 l2 = __floats2bfloat162_rn(v[j] - __low2float(h2), v[j + 1] - __high2float(h2));
+          hp[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          lp[j >> 1] = *reinterpret_cast<uint32_t*>(&l2);
+        }
         if (fast) {
-          store_bf16(stage, out_hi, row0, col0, hi);
-          if (out_lo) store_bf16(stage, out_lo, row0, col0, lo);
+          store_bf16(stage, out_hi, row0, col0, hp);
+          if (out_lo) store_bf16(stage, out_lo, row0, col0, lp);
         } else if (row_ok) {
-          __nv_bfloat16* hp = out_hi + (size_t)row * ld_bf + col0;
-          __nv_bfloat16* lp = out_lo ? out_lo + (size_t)row * ld_bf + col0 : nullptr;
-          for (int j = 0; j < 32; ++j)
+          __nv_bfloat16* hq = out_hi + (size_t)row * ld_bf + col0;
+          __nv_bfloat16* lq = out_lo ? out_lo + (size_t)row * ld_bf + col0 : nullptr;
+          const __nv_bfloat16* hs = reinterpret_cast<const __nv_bfloat16*>(hp);
+          const __nv_bfloat16* ls = reinterpret_cast<const __nv_bfloat16*>(lp);
+          for (int j = 0; j < 16; ++j)
             if (col0 + j < N) {
-              hp[j] = hi[j];
-              if (lp) lp[j] = lo[j];
+              hq[j] = hs[j];
+              if (lq) lq[j] = ls[j];
             }
         }
       }
@@ -242,7 +251,7 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                   reinterpret_cast<__nv_bfloat16*>(out_lo), ld_bf, gelu, 0, vec};
   cudaStream_t s = as_stream(stream);
   if (passes == 1) {
-    if (BN == 256) return launch_std<256, 1, 4>(ta, talo, tb, tblo, M, N, K, epi, s);
+    if (BN == 256) return launch_std<256, 1, 4>(ta, talo, tb, tblo, M, N, K, epi, s);  // 230 KB
     if (BN == 192) return launch_std<192, 1, 4>(ta, talo, tb, tblo, M, N, K, epi, s);
     return launch_std<128, 1, 6>(ta, talo, tb, tblo, M, N, K, epi, s);
   }

@@ -21,9 +21,10 @@ namespace astra {
 constexpr int kBM = 128;  // UMMA M (rows per tile)
 constexpr int kBK = 64;   // bf16 elements per 128-byte swizzle row
 constexpr int kUK = 16;   // UMMA K for kind::f16
-constexpr int kEpiWarps = 8;      // two warps per TMEM lane quarter, each owns half the columns
+constexpr int kEpiWarps = 16;     // four warps per TMEM lane quarter, each owns 1/4 of the columns
+constexpr int kEpiParts = kEpiWarps / 4;
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
-constexpr int kEpiStageBytes = 4096 + 128;  // per-epilogue-warp smem: 32x32 fp32 tile + 32 floats
+constexpr int kEpiStageBytes = 2048 + 64;   // per-epilogue-warp smem: 32x16 fp32 tile + 16 floats
 
 template <int BN, int PASSES>
 struct GemmSmem {
@@ -61,7 +62,8 @@ struct TileSched {
 // Epi must provide:
 //   __device__ void operator()(const TileCoord&, int row_in_tile /*0..127*/,
 //                              uint32_t tmem_row_addr /*lane-qualified TMEM address of col 0*/,
-//                              int col_begin, int col_end /*this warp's column half*/,
+//                              int col_begin, int col_end, int part /*this warp's column
+//                              quarter (BN/4 columns)*/,
 //                              uint8_t* stage /*kEpiStageBytes of warp-private smem*/) const;
 // It reads its accumulator row via tmem_ld32 (warp-collective) and writes results.
 template <int BN, int PASSES, int STAGES, class Epi>
@@ -186,8 +188,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // -------------------------------------------------------------- epilogue
     const uint32_t quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
-    const int half = (warp - 2) / 4;
-    const int col_begin = half * (BN / 2), col_end = col_begin + BN / 2;
+    const int part = (warp - 2) / 4;
+    const int col_begin = part * (BN / kEpiParts), col_end = col_begin + BN / kEpiParts;
     uint8_t* stage = epi_stage + (warp - 2) * kEpiStageBytes;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;
-      epi(tc, row_in_tile, taddr, col_begin, col_end, stage);
+      epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {

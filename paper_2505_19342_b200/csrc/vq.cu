@@ -42,7 +42,7 @@ struct VqWorkspace {
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
-  const int nchunk = 2 * ((K + kVqBN - 1) / kVqBN);
+  const int nchunk = kEpiParts * ((K + kVqBN - 1) / kVqBN);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -148,13 +148,13 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
 
 // ---------------------------------------------------------- epilogue
 struct VqEpilogue {
-  int M, K, nchunk;         // nchunk = records per (g, row) = 2 per 256-code tile (column halves)
+  int M, K, nchunk;         // nchunk = records per (g, row): kEpiParts per 256-code tile
   const float* c_sq;        // [G, K]
   const float* c_norm_max;  // [G]
   VqWorkspace w;
 
   __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
-                                             int cb, int ce, uint8_t* stage) const {
+                                             int cb, int ce, int part, uint8_t* stage) const {
     const int row = tc.m_blk * kBM + row_in_tile;
     const bool ok = row < M;
     const int g = tc.batch;
@@ -188,7 +188,7 @@ struct VqEpilogue {
     best = fminf(fminf(bst[0], bst[1]), fminf(bst[2], bst[3]));
     const float xn = ok ? w.x_norm[(size_t)g * M + row] : 0.f;
     const float thr = best + 2.0f * score_delta(xn, __ldg(c_norm_max + g));
-    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk * 2 + (cb > 0 ? 1 : 0);
+    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk * kEpiParts + part;
     int cnt = 0;
 #pragma unroll 1
     for (int c0 = cb; c0 < ce; c0 += 32) {
@@ -416,7 +416,7 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
                             cudaStream_t s) {
   const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
   const int ntile = (K + kVqBN - 1) / kVqBN;
-  const int nchunk = 2 * ntile;
+  const int nchunk = kEpiParts * ntile;   // one record per epilogue column part
   CUtensorMap ta, talo, tb, tblo;
   int st;
   if ((st = make_tmap_2d(&ta, a_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * Mg, gdp,
