@@ -330,47 +330,63 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
     phase ^= 1;
     tc_fence_after();
 
-    // ---- softmax of row r over this chunk.  Non-causal: only the chunk tail is masked
-    // (uniform bound); causal: key_pos <= query position, replica keys (pos -1) visible.
+    // ---- softmax of row r over this chunk, branch-free: a 32-bit visibility mask per
+    // 32-column group (non-causal: only the chunk tail; causal: key_pos <= query position,
+    // replica keys have position -1) turns masked scores into -inf, so max and exp2 need no
+    // control flow and masked weights come out exactly 0.
     const int valid = min(kTK, nk - kc);
-    float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll 1
-    for (int cc = 0; cc < 4; ++cc) {
-      if (cc * 32 >= valid) break;
-      uint32_t rr[32];
-      tmem_ld32(tS + lane_off + cc * 32, rr);
-      tmem_ld_wait();
-      const bool full = !a.causal && (cc * 32 + 32 <= valid);
+    uint32_t vm[4];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = cc * 32 + j;
-        const bool vis = full || (col < valid && (!a.causal || kpos[col] <= qpos));
-        if (vis) mx[j & 3] = fmaxf(mx[j & 3], __uint_as_float(rr[j]));
+    for (int cc = 0; cc < 4; ++cc) {
+      const int left = valid - cc * 32;
+      uint32_t m32 = left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u));
+      if (a.causal && m32) {
+        uint32_t c32 = 0;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const short2 kp2 = *reinterpret_cast<const short2*>(kpos + cc * 32 + j);
+          c32 |= (uint32_t)(kp2.x <= qpos) << j;
+          c32 |= (uint32_t)(kp2.y <= qpos) << (j + 1);
+        }
+        m32 &= c32;
+      }
+      vm[cc] = m32;
+    }
+    const int ngroups = (valid + 31) >> 5;
+    float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      if (cc < ngroups) {
+        uint32_t rr[32];
+        tmem_ld32(tS + lane_off + cc * 32, rr);
+        tmem_ld_wait();
+        const uint32_t m32 = vm[cc];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY;
+          mx[j & 3] = fmaxf(mx[j & 3], x);
+        }
       }
     }
     const float cmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
     const float mnew = fmaxf(m, cmax * sl2);
     const float corr = (m == -INFINITY) ? 0.f : ex2_approx(m - mnew);
+    const float mref = (mnew == -INFINITY) ? 0.f : mnew;  // fully masked so far: all p = 0
     float ls[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 1
+#pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
-      uint4* prow = nullptr;
       uint32_t pk[16];
-      if (cc * 32 < valid) {
+      if (cc < ngroups) {
         uint32_t rr[32];
         tmem_ld32(tS + lane_off + cc * 32, rr);
         tmem_ld_wait();
-        const bool full = !a.causal && (cc * 32 + 32 <= valid);
+        const uint32_t m32 = vm[cc];
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
-          float p2[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int col = cc * 32 + j + u;
-            const bool vis = full || (col < valid && (!a.causal || kpos[col] <= qpos));
-            p2[u] = vis ? ex2_approx(fmaf(__uint_as_float(rr[j + u]), sl2, -mnew)) : 0.f;
-          }
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p2[0], p2[1]);
+          const float x0 = ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY;
+          const float x1 = ((m32 >> (j + 1)) & 1u) ? __uint_as_float(rr[j + 1]) : -INFINITY;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(ex2_approx(fmaf(x0, sl2, -mref)),
+                                                    ex2_approx(fmaf(x1, sl2, -mref)));
           // sum what the tensor core multiplies (the bf16-rounded probabilities)
           ls[(j >> 1) & 3] += __low2float(b2) + __high2float(b2);
           pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
@@ -387,7 +403,6 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
         *reinterpret_cast<uint4*>(blk + sw128_offset(r, chunk)) =
             make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
       }
-      (void)prow;
     }
     l = l * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
     m = mnew;

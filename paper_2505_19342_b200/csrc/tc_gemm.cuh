@@ -44,17 +44,19 @@ struct TileCoord {
   int m_blk, n_blk, batch;
 };
 
-// Tile scheduler: tiles enumerate (batch, n_blk, m_blk) with m fastest so that
-// consecutive CTAs share the same B tile (weights / codebook chunk) in L2.
+// Tile scheduler: tiles enumerate (batch, m_blk, n_blk) with n fastest.  B (weights, a
+// codebook) is a few MB and stays L2-resident; A (activations, up to ~80 MB) is the stream,
+// so the CTAs that share an A row-block run concurrently and A crosses HBM once
+// (m-fastest order re-read the 77 MB W2 operand from DRAM once per column tile).
 struct TileSched {
   int num_m, num_n, num_b;
   __device__ int total() const { return num_m * num_n * num_b; }
   __device__ TileCoord get(int t) const {
     TileCoord c;
-    c.m_blk = t % num_m;
-    t /= num_m;
     c.n_blk = t % num_n;
-    c.batch = t / num_n;
+    t /= num_n;
+    c.m_blk = t % num_m;
+    c.batch = t / num_m;
     return c;
   }
 };
