@@ -295,7 +295,15 @@ def main():
     torch.cuda.synchronize()
 
     # ---- per-kernel event timing (same kernels, eager, after the timed region)
-    prof = _profile(rt)
+    rt.vq_stats.zero_()
+    prof = _profile(rt, steps=3)
+    vs = rt.vq_stats.cpu().numpy().astype(float) / 3.0
+    tokens_encoded = rt.n_content * L
+    vq_stats = {"tokens_encoded_per_step": tokens_encoded,
+                "tokens_reranked_fp64": vs[0] + vs[1], "tokens_with_overflowed_chunk": vs[1],
+                "window_candidates_per_token": round(vs[2] / max(tokens_encoded, 1), 4),
+                "window": "|x.c error| <= 2^-14 ||x|| max||c|| (bf16x3 representation bound "
+                          "3.02*2^-16 + fp32 accumulation headroom)"}
     work = _kernel_work(rt)
     step_ms_eager = sum(v["total_ms"] for v in prof.values())
     kernels = {}
@@ -374,6 +382,7 @@ def main():
             "roofline": roof,
             "kernels": kernels,
             "vq_encode_gbs": vq.get("achieved_gbs"),
+            "vq_exactness": vq_stats,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},

@@ -44,7 +44,8 @@ int astra_abi_version(void);
  *
  *   v[m, n]  = sum_k A[m, k] * B[n, k]        (B is the weight TRANSPOSED: [N, K])
  *   v       += bias[n]            (bias != NULL)
- *   v        = gelu_erf(v)        (gelu != 0)
+ *   v        = gelu_erf(v)        (gelu = 1: fp32-class, |err| < 4e-7;
+ *                                  gelu = 2: bf16-output class, |err| < 3e-5)
  *   v        = residual[m, n] + v (residual != NULL)
  *   out_f32[m, n] = v; out_hi/out_lo[m, n] = bf16 split of v (each optional)
  *

@@ -212,24 +212,39 @@ __device__ __forceinline__ void cp_async_wait_group() {
 }
 
 // Issue the cp.async gather of key chunk [kc, kc+128) into (sK, sV) and its positions.
-__device__ __forceinline__ void attn_load_chunk(const AttnArgs& a, int kc, int k0, int nk,
-                                                int hoff, uint32_t k_s, uint32_t v_s,
-                                                uint8_t* sK, uint8_t* sV, short* kpos, int tid) {
-  const __nv_bfloat16* KL = reinterpret_cast<const __nv_bfloat16*>(a.k_local);
-  const __nv_bfloat16* VL = reinterpret_cast<const __nv_bfloat16*>(a.v_local);
-  const __nv_bfloat16* KR = reinterpret_cast<const __nv_bfloat16*>(a.k_remote);
-  const __nv_bfloat16* VR = reinterpret_cast<const __nv_bfloat16*>(a.v_remote);
-  // one key row per thread: a single key_src load, then 2 x 8 16-byte async copies
-  const int key = kc + tid;
+// Key descriptor of key `key` of the segment (loaded ahead of use: src < 0 marks a remote
+// (codebook-table) row, INT_MIN a padding key).
+struct KeyRef {
+  int src;
+  short pos;
+};
+__device__ __forceinline__ KeyRef attn_key_ref(const AttnArgs& a, int k0, int nk, int key) {
+  KeyRef r;
   if (key < nk) {
-    const int src = __ldg(a.key_src + k0 + key);
+    r.src = __ldg(a.key_src + k0 + key);
+    r.pos = a.causal ? (short)__ldg(a.key_pos + k0 + key) : (short)0;
+  } else {
+    r.src = INT_MIN;
+    r.pos = kPosNever;
+  }
+  return r;
+}
+
+// Issue the cp.async gather of one key row per thread (2 x 8 16-byte copies) into the chunk
+// buffers (sK, sV) and record its position; padding keys are zero-filled.
+__device__ __forceinline__ void attn_load_chunk(const AttnArgs& a, KeyRef kr, int hoff,
+                                                uint32_t k_s, uint32_t v_s, uint8_t* sK,
+                                                uint8_t* sV, short* kpos, int tid) {
+  if (kr.src != INT_MIN) {
     const __nv_bfloat16 *kp, *vp;
-    if (src >= 0) {
-      kp = KL + (size_t)src * a.ld_local + hoff;
-      vp = VL + (size_t)src * a.ld_local + hoff;
+    if (kr.src >= 0) {
+      kp = reinterpret_cast<const __nv_bfloat16*>(a.k_local) + (size_t)kr.src * a.ld_local + hoff;
+      vp = reinterpret_cast<const __nv_bfloat16*>(a.v_local) + (size_t)kr.src * a.ld_local + hoff;
     } else {
-      kp = KR + (size_t)(-(src + 1)) * a.ld_remote + hoff;
-      vp = VR + (size_t)(-(src + 1)) * a.ld_remote + hoff;
+      kp = reinterpret_cast<const __nv_bfloat16*>(a.k_remote) +
+           (size_t)(-(kr.src + 1)) * a.ld_remote + hoff;
+      vp = reinterpret_cast<const __nv_bfloat16*>(a.v_remote) +
+           (size_t)(-(kr.src + 1)) * a.ld_remote + hoff;
     }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
@@ -243,7 +258,7 @@ __device__ __forceinline__ void attn_load_chunk(const AttnArgs& a, int kc, int k
       *reinterpret_cast<uint4*>(sV + sw128_offset(tid, c)) = make_uint4(0, 0, 0, 0);
     }
   }
-  kpos[tid] = (kc + tid < nk) ? (short)__ldg(a.key_pos + k0 + kc + tid) : kPosNever;
+  kpos[tid] = kr.pos;
 }
 
 __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
@@ -272,6 +287,9 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
     fence_barrier_init();
   }
   const uint32_t q_s = smem_u32(sQ), p_s = smem_u32(sP);
+  // key descriptors of the first two chunks: loads issued now, consumed after the Q copies
+  const KeyRef kr0 = attn_key_ref(a, k0, nk, tid);
+  const KeyRef kr1 = attn_key_ref(a, k0, nk, kTK + tid);
   // prologue: group 0 = Q + key chunk 0, group 1 = key chunk 1
   {
     const int qr = qt * kTQ + tid;  // one query row per thread
@@ -286,11 +304,11 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
     }
   }
   const int nchunks = (nk + kTK - 1) / kTK;
-  attn_load_chunk(a, 0, k0, nk, hoff, smem_u32(sK0), smem_u32(sV0), sK0, sV0, sKpos, tid);
+  attn_load_chunk(a, kr0, hoff, smem_u32(sK0), smem_u32(sV0), sK0, sV0, sKpos, tid);
   cp_async_commit();
   if (nchunks > 1)
-    attn_load_chunk(a, kTK, k0, nk, hoff, smem_u32(sK0 + 16384), smem_u32(sV0 + 16384),
-                    sK0 + 16384, sV0 + 16384, sKpos + 128, tid);
+    attn_load_chunk(a, kr1, hoff, smem_u32(sK0 + 16384), smem_u32(sV0 + 16384), sK0 + 16384,
+                    sV0 + 16384, sKpos + 128, tid);
   cp_async_commit();
   tc_fence_before();
   __syncthreads();
@@ -435,8 +453,8 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
     tc_fence_before();
     __syncthreads();   // buffers of this chunk are free
     if (c + 2 < nchunks)
-      attn_load_chunk(a, (c + 2) * kTK, k0, nk, hoff, smem_u32(sK), smem_u32(sV), sK, sV,
-                      sKpos + buf * 128, tid);
+      attn_load_chunk(a, attn_key_ref(a, k0, nk, (c + 2) * kTK + tid), hoff, smem_u32(sK),
+                      smem_u32(sV), sK, sV, sKpos + buf * 128, tid);
     cp_async_commit();
   }
 

@@ -85,9 +85,12 @@ struct StdEpilogue {
         }
         __syncwarp();
       }
-      if (gelu) {
+      if (gelu == 1) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = gelu_erf(v[j]);
+      } else if (gelu == 2) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = gelu_erf_bf16(v[j]);
       }
       if (residual) {
         if (fast) {

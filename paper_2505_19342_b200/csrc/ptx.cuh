@@ -223,4 +223,23 @@ ASTRA_DEVICE float gelu_erf(float x) {
   return x * (x >= 0.0f ? 1.0f - h : h);
 }
 
+// Same construction with a degree-8 R (max |error| 2.7e-5, relative 2.7e-4 where |gelu| >
+// 1e-2): for the bf16 fast path, whose output rounding (3.9e-3 relative) dominates.
+ASTRA_DEVICE float gelu_erf_bf16(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float e = exp2f(-(z * z) * 1.4426950408889634f);
+  const float u = fminf(z, 4.0f) - 2.0f;
+  float r = 0.00013683406605387587f;
+  r = fmaf(r, u, -0.00043860508011060994f);
+  r = fmaf(r, u, 0.00025942515572788624f);
+  r = fmaf(r, u, -0.0009406567103610213f);
+  r = fmaf(r, u, 0.005955796716703947f);
+  r = fmaf(r, u, -0.01653105315666264f);
+  r = fmaf(r, u, 0.041532531022877815f);
+  r = fmaf(r, u, -0.10645975582795f);
+  r = fmaf(r, u, 0.2554180079701582f);
+  const float h = 0.5f * e * r;
+  return x * (x >= 0.0f ? 1.0f - h : h);
+}
+
 }  // namespace astra

@@ -288,27 +288,31 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
     const double* cc = cb.c_sq64 + (size_t)g * K;
     double bd = INFINITY;
     int bi = -1;
-    if (overflow) {
-      for (int k = 0; k < K; ++k) {
-        const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
-        if (d < bd) {
-          bd = d;
-          bi = k;
-        }
-      }
-    } else {
-      // candidates in increasing code order (chunks ascending, columns ascending)
-      for (int c = 0; c < nchunk; ++c) {
-        if (w.rec_best[rec0 + c] > thr) continue;
-        const int m = w.rec_cnt[rec0 + c];
-        for (int i = 0; i < m; ++i) {
-          if (w.rec_score[(rec0 + c) * kVqCap + i] > thr) continue;
-          const int k = w.rec_idx[(rec0 + c) * kVqCap + i];
+    // candidates in increasing code order; a chunk whose list overflowed contributes all of
+    // its codes (chunk c = tile c / kEpiParts, column part c % kEpiParts: 64 codes)
+    constexpr int kPartCodes = kVqBN / kEpiParts;
+    for (int c = 0; c < nchunk; ++c) {
+      if (w.rec_best[rec0 + c] > thr) continue;
+      const int m = w.rec_cnt[rec0 + c];
+      if (m > kVqCap) {
+        const int k_lo = (c / kEpiParts) * kVqBN + (c % kEpiParts) * kPartCodes;
+        const int k_hi = min(K, k_lo + kPartCodes);
+        for (int k = k_lo; k < k_hi; ++k) {
           const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
           if (d < bd || (d == bd && k < bi)) {
             bd = d;
             bi = k;
           }
+        }
+        continue;
+      }
+      for (int i = 0; i < m; ++i) {
+        if (w.rec_score[(rec0 + c) * kVqCap + i] > thr) continue;
+        const int k = w.rec_idx[(rec0 + c) * kVqCap + i];
+        const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
+        if (d < bd || (d == bd && k < bi)) {
+          bd = d;
+          bi = k;
         }
       }
     }

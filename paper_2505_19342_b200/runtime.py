@@ -93,6 +93,7 @@ class AstraRuntime:
         self.cfg, self.plan, self.B = cfg, plan, int(batch)
         self.mode, self.cls_mode, self.precision = mode, cls_mode, precision
         self.fast = precision == "fast"
+        self.gelu_mode = 2 if self.fast else 1   # astra_gemm: 2 = bf16-class GELU polynomial
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.comm = comm
         self.D, self.H, self.L = cfg.hidden, cfg.heads, cfg.layers
@@ -407,7 +408,7 @@ class AstraRuntime:
                      _p(self.ln_lo), D, s)
         whi, wlo = lay["w1"]
         with self._op("gemm_w1"):
-            kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo, bias=lay["b1"], gelu=True,
+            kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo, bias=lay["b1"], gelu=self.gelu_mode,
                          out_hi=self.f_hi, out_lo=self.f_lo)
         whi, wlo = lay["w2"]
         with self._op("gemm_w2"):
@@ -604,7 +605,7 @@ class AstraRuntime:
             _native.call("astra_layernorm", H.data_ptr(), B, D, D, lay["ln2_g"].data_ptr(),
                          lay["ln2_b"].data_ptr(), LN_EPS, None, 0, self.dec_ln_hi.data_ptr(),
                          _p(self.dec_ln_lo), D, s)
-            self._gemm_rows(lay["w1"], self.dec_ln_hi, self.dec_ln_lo, bias=lay["b1"], gelu=True,
+            self._gemm_rows(lay["w1"], self.dec_ln_hi, self.dec_ln_lo, bias=lay["b1"], gelu=self.gelu_mode,
                             out_hi=self.dec_f_hi, out_lo=self.dec_f_lo)
             self._gemm_rows(lay["w2"], self.dec_f_hi, self.dec_f_lo, bias=lay["b2"], residual=H,
                             out_f32=X)
