@@ -165,24 +165,27 @@ struct StdEpilogue {
   }
 };
 
-template <int BN, int PASSES, int STAGES>
+// Deepest operand ring that fits next to the epilogue staging (<= 192 KB of stages).
+template <int BN, int PASSES, int CLUSTER>
+constexpr int gemm_stages() {
+  constexpr int per = GemmSmem<BN, PASSES, CLUSTER>::kStageBytes;
+  constexpr int n = 196608 / per;
+  return n > 8 ? 8 : n;
+}
+
+template <int BN, int PASSES>
 static int launch_std(const CUtensorMap& ta, const CUtensorMap& talo, const CUtensorMap& tb,
                       const CUtensorMap& tblo, int M, int N, int K, StdEpilogue epi,
-                      cudaStream_t stream) {
-  auto kern = tc_gemm_kernel<BN, PASSES, STAGES, StdEpilogue>;
-  constexpr int smem = gemm_smem_bytes<BN, PASSES, STAGES>();
-  static_assert(smem <= 232448, "GEMM smem budget exceeded");
-  static bool configured = false;
-  if (!configured) {
-    ASTRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
-  TileSched sched{(M + kBM - 1) / kBM, (N + BN - 1) / BN, 1};
-  const int tiles = sched.num_m * sched.num_n;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+                      cudaStream_t stream, int cluster) {
+  TileSched sched{(M + kBM - 1) / kBM, (N + BN - 1) / BN, 1, 1};
   epi.BN = BN;
-  kern<<<grid, kGemmThreads, smem, stream>>>(ta, talo, tb, tblo, K, sched, 0, 0, epi);
-  ASTRA_CUDA_CHECK(cudaGetLastError());
+  const cudaError_t e =
+      cluster == 2
+          ? launch_tc_gemm<BN, PASSES, gemm_stages<BN, PASSES, 2>(), 2>(
+                ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms())
+          : launch_tc_gemm<BN, PASSES, gemm_stages<BN, PASSES, 1>(), 1>(
+                ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms());
+  ASTRA_CUDA_CHECK(e);
   return ASTRA_OK;
 }
 
@@ -227,17 +230,21 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
   ASTRA_REQUIRE(out_lo == nullptr || out_hi != nullptr, ASTRA_ERR_SHAPE,
                 "astra_gemm: out_lo requires out_hi");
   const int BN = pick_bn(M, N);
+  // pairs of CTAs share (multicast) the B tile whenever there are two row blocks to pair
+  const int cluster = (M > kBM) ? 2 : 1;
+  const int brows = BN / cluster;
   CUtensorMap ta, talo, tb, tblo;
   int st;
   if ((st = make_tmap_2d(&ta, a_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, lda, kBM, kBK, true)))
     return st;
-  if ((st = make_tmap_2d(&tb, b_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, K, ldb, BN, kBK, true)))
+  if ((st = make_tmap_2d(&tb, b_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, K, ldb, brows, kBK,
+                         true)))
     return st;
   if (passes == 3) {
     if ((st = make_tmap_2d(&talo, a_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, lda, kBM, kBK,
                            true)))
       return st;
-    if ((st = make_tmap_2d(&tblo, b_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, K, ldb, BN, kBK,
+    if ((st = make_tmap_2d(&tblo, b_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, K, ldb, brows, kBK,
                            true)))
       return st;
   } else {
@@ -254,11 +261,11 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                   reinterpret_cast<__nv_bfloat16*>(out_lo), ld_bf, gelu, 0, vec};
   cudaStream_t s = as_stream(stream);
   if (passes == 1) {
-    if (BN == 256) return launch_std<256, 1, 4>(ta, talo, tb, tblo, M, N, K, epi, s);  // 230 KB
-    if (BN == 192) return launch_std<192, 1, 4>(ta, talo, tb, tblo, M, N, K, epi, s);
-    return launch_std<128, 1, 6>(ta, talo, tb, tblo, M, N, K, epi, s);
+    if (BN == 256) return launch_std<256, 1>(ta, talo, tb, tblo, M, N, K, epi, s, cluster);  // 230 KB
+    if (BN == 192) return launch_std<192, 1>(ta, talo, tb, tblo, M, N, K, epi, s, cluster);
+    return launch_std<128, 1>(ta, talo, tb, tblo, M, N, K, epi, s, cluster);
   }
-  if (BN == 256) return launch_std<256, 3, 2>(ta, talo, tb, tblo, M, N, K, epi, s);
-  if (BN == 192) return launch_std<192, 3, 2>(ta, talo, tb, tblo, M, N, K, epi, s);
-  return launch_std<128, 3, 3>(ta, talo, tb, tblo, M, N, K, epi, s);
+  if (BN == 256) return launch_std<256, 3>(ta, talo, tb, tblo, M, N, K, epi, s, cluster);
+  if (BN == 192) return launch_std<192, 3>(ta, talo, tb, tblo, M, N, K, epi, s, cluster);
+  return launch_std<128, 3>(ta, talo, tb, tblo, M, N, K, epi, s, cluster);
 }

@@ -26,17 +26,19 @@ constexpr int kEpiParts = kEpiWarps / 4;
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiStageBytes = 2048 + 64;   // per-epilogue-warp smem: 32x16 fp32 tile + 16 floats
 
-template <int BN, int PASSES>
+// Per-CTA smem stage: A tile (128 rows) and this CTA's share of the B tile (all BN rows,
+// or BN/2 when a CTA pair splits B across its two SMs), times 2 for the bf16x3 lo operands.
+template <int BN, int PASSES, int CLUSTER = 1>
 struct GemmSmem {
   static constexpr int kATile = kBM * kBK * 2;       // bytes
-  static constexpr int kBTile = BN * kBK * 2;
+  static constexpr int kBTile = (BN / CLUSTER) * kBK * 2;
   static constexpr int kOperands = (PASSES == 3) ? 2 : 1;
   static constexpr int kStageBytes = kOperands * (kATile + kBTile);
 };
 
-template <int BN, int PASSES, int STAGES>
+template <int BN, int PASSES, int STAGES, int CLUSTER = 1>
 constexpr int gemm_smem_bytes() {
-  return STAGES * GemmSmem<BN, PASSES>::kStageBytes + kEpiWarps * kEpiStageBytes +
+  return STAGES * GemmSmem<BN, PASSES, CLUSTER>::kStageBytes + kEpiWarps * kEpiStageBytes +
          1024 /*align*/ + 256 /*barriers*/;
 }
 
@@ -50,13 +52,16 @@ struct TileCoord {
 // (m-fastest order re-read the 77 MB W2 operand from DRAM once per column tile).
 struct TileSched {
   int num_m, num_n, num_b;
-  __device__ int total() const { return num_m * num_n * num_b; }
-  __device__ TileCoord get(int t) const {
+  int cluster;  // CTAs per cluster along M (1 or 2); a unit = `cluster` adjacent row blocks
+  __device__ int num_units_m() const { return (num_m + cluster - 1) / cluster; }
+  __device__ int total() const { return num_units_m() * num_n * num_b; }
+  __device__ TileCoord get(int t, int rank) const {
     TileCoord c;
     c.n_blk = t % num_n;
     t /= num_n;
-    c.m_blk = t % num_m;
-    c.batch = t / num_m;
+    const int mu = num_units_m();
+    c.m_blk = (t % mu) * cluster + rank;
+    c.batch = t / mu;
     return c;
   }
 };
@@ -67,13 +72,24 @@ struct TileSched {
 //                              int col_begin, int col_end, int part /*this warp's column
 //                              quarter (BN/4 columns)*/,
 //                              uint8_t* stage /*kEpiStageBytes of warp-private smem*/) const;
-// It reads its accumulator row via tmem_ld32 (warp-collective) and writes results.
-template <int BN, int PASSES, int STAGES, class Epi>
+// It reads its accumulator row via tmem_ld* (warp-collective) and writes results.
+//
+// CLUSTER == 2: a CTA pair (cta_group::2).  The two CTAs of a cluster own adjacent 128-row
+// blocks of one 256-row tile; each loads its A rows and HALF of the B tile into its own smem,
+// and the leader (even rank) issues M=256 UMMAs that read both CTAs' operands and write each
+// CTA's TMEM rows.  Per SM the operand traffic drops from (128 + BN) to (128 + BN/2) rows per
+// k-step — these GEMMs are bound by L2->SM bandwidth (~6.3 KB/clk chip-wide), not by the
+// tensor pipe.  Barriers: the leader's full barrier counts both CTAs' TMA bytes; its MMA
+// commits (multicast) release the stage / publish the accumulator in both CTAs; both CTAs'
+// epilogue warps arrive on the leader's TMEM-empty barrier.
+template <int BN, int PASSES, int STAGES, int CLUSTER, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo,
                    int K, TileSched sched, int a_batch_rows, int b_batch_rows, Epi epi) {
-  using S = GemmSmem<BN, PASSES>;
+  using S = GemmSmem<BN, PASSES, CLUSTER>;
+  static_assert(CLUSTER == 1 || CLUSTER == 2, "cluster of 1 or 2");
+  constexpr bool kPair = CLUSTER == 2;
   constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                  : (2 * BN <= 256) ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -88,6 +104,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  const int rank = kPair ? (int)cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int unit0 = blockIdx.x / CLUSTER, units = gridDim.x / CLUSTER;
   const int num_kb = (K + kBK - 1) / kBK;
   const int total = sched.total();
 
@@ -104,36 +123,58 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 32 * kEpiWarps);
+      mbar_init(&tempty_bar[s], kPair ? 2 * kEpiWarps : 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if (kPair)
+      tmem_alloc_pair<kTmemCols>(tmem_slot);
+    else
+      tmem_alloc<kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    cluster_sync();  // the peer touches our barriers / TMEM only after they exist
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ------------------------------------------------------------ producer
+      // ------------------------------------------------------------ producer (both CTAs)
+      const uint32_t full0 = kPair ? mapa_shared(full_bar, 0) : smem_u32(full_bar);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        TileCoord tc = sched.get(t);
+      for (int t = unit0; t < total; t += units) {
+        TileCoord tc = sched.get(t, rank);
         const int arow = tc.batch * a_batch_rows + tc.m_blk * kBM;
-        const int brow = tc.batch * b_batch_rows + tc.n_blk * BN;
+        const int brow = tc.batch * b_batch_rows + tc.n_blk * BN + rank * (BN / CLUSTER);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * S::kStageBytes;
-          mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
-          tma_load_2d(st, &tmA, &full_bar[stage], kb * kBK, arow, kEvictNormal);
-          tma_load_2d(st + S::kATile, &tmB, &full_bar[stage], kb * kBK, brow, kEvictLast);
-          if (PASSES == 3) {
-            tma_load_2d(st + S::kATile + S::kBTile, &tmAlo, &full_bar[stage], kb * kBK, arow,
-                        kEvictNormal);
-            tma_load_2d(st + 2 * S::kATile + S::kBTile, &tmBlo, &full_bar[stage], kb * kBK, brow,
-                        kEvictLast);
+          const int kc = kb * kBK;
+          if (kPair) {
+            // both CTAs' bytes land on the leader's full barrier
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+            const uint32_t fb = full0 + stage * 8;
+            tma_load_2d_pair(st, &tmA, fb, kc, arow, kEvictNormal);
+            tma_load_2d_pair(st + S::kATile, &tmB, fb, kc, brow, kEvictLast);
+            if (PASSES == 3) {
+              tma_load_2d_pair(st + S::kATile + S::kBTile, &tmAlo, fb, kc, arow, kEvictNormal);
+              tma_load_2d_pair(st + 2 * S::kATile + S::kBTile, &tmBlo, fb, kc, brow, kEvictLast);
+            }
+          } else {
+            mbar_arrive_expect_tx(&full_bar[stage], S::kStageBytes);
+            tma_load_2d(st, &tmA, &full_bar[stage], kc, arow, kEvictNormal);
+            tma_load_2d(st + S::kATile, &tmB, &full_bar[stage], kc, brow, kEvictLast);
+            if (PASSES == 3) {
+              tma_load_2d(st + S::kATile + S::kBTile, &tmAlo, &full_bar[stage], kc, arow,
+                          kEvictNormal);
+              tma_load_2d(st + 2 * S::kATile + S::kBTile, &tmBlo, &full_bar[stage], kc, brow,
+                          kEvictLast);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -143,14 +184,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(kBM, BN);
+    if (lane == 0 && leader) {
+      // ------------------------------------------------------------ MMA issuer (leader)
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM * CLUSTER, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = unit0; t < total; t += units) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -164,22 +205,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int kk = 0; kk < kBK / kUK; ++kk) {
             const uint32_t koff = kk * kUK * 2;  // bytes inside the 128B swizzle row
             const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
-            umma_f16(d_tmem, sdesc_kmajor_sw128(a_hi + koff), sdesc_kmajor_sw128(b_hi + koff), idesc,
-                     accum);
-            if (PASSES == 3) {
-              umma_f16(d_tmem, sdesc_kmajor_sw128(a_hi + koff), sdesc_kmajor_sw128(b_lo + koff),
-                       idesc, 1u);
-              umma_f16(d_tmem, sdesc_kmajor_sw128(a_lo + koff), sdesc_kmajor_sw128(b_hi + koff),
-                       idesc, 1u);
+            if (kPair) {
+              umma_f16_pair(d_tmem, sdesc_kmajor_sw128(a_hi + koff),
+                            sdesc_kmajor_sw128(b_hi + koff), idesc, accum);
+              if (PASSES == 3) {
+                umma_f16_pair(d_tmem, sdesc_kmajor_sw128(a_hi + koff),
+                              sdesc_kmajor_sw128(b_lo + koff), idesc, 1u);
+                umma_f16_pair(d_tmem, sdesc_kmajor_sw128(a_lo + koff),
+                              sdesc_kmajor_sw128(b_hi + koff), idesc, 1u);
+              }
+            } else {
+              umma_f16(d_tmem, sdesc_kmajor_sw128(a_hi + koff), sdesc_kmajor_sw128(b_hi + koff),
+                       idesc, accum);
+              if (PASSES == 3) {
+                umma_f16(d_tmem, sdesc_kmajor_sw128(a_hi + koff), sdesc_kmajor_sw128(b_lo + koff),
+                         idesc, 1u);
+                umma_f16(d_tmem, sdesc_kmajor_sw128(a_lo + koff), sdesc_kmajor_sw128(b_hi + koff),
+                         idesc, 1u);
+              }
             }
           }
-          umma_commit(&empty_bar[stage]);  // smem slot free once these MMAs retire
+          // the smem slot is free once these MMAs retire (in both CTAs of a pair)
+          if (kPair)
+            umma_commit_pair_mc(&empty_bar[stage], 0x3);
+          else
+            umma_commit(&empty_bar[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue (of both CTAs)
+        if (kPair)
+          umma_commit_pair_mc(&tfull_bar[acc], 0x3);
+        else
+          umma_commit(&tfull_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -187,22 +247,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // -------------------------------------------------------------- epilogue
+    // -------------------------------------------------------------- epilogue (both CTAs)
     const uint32_t quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
     const int part = (warp - 2) / 4;
     const int col_begin = part * (BN / kEpiParts), col_end = col_begin + BN / kEpiParts;
     uint8_t* stage = epi_stage + (warp - 2) * kEpiStageBytes;
+    const uint32_t tempty0 = kPair ? mapa_shared(tempty_bar, 0) : 0u;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      TileCoord tc = sched.get(t);
+    for (int t = unit0; t < total; t += units) {
+      TileCoord tc = sched.get(t, rank);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;
       epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage);
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if (kPair) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + acc * 8);  // one arrival per warp
+      } else {
+        mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -210,11 +276,54 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
 
-  __syncthreads();
+  tc_fence_before();
+  if (kPair)
+    cluster_sync();  // no CTA leaves (or frees TMEM) while its peer may still use the pair
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
+    if (kPair)
+      tmem_dealloc_pair<kTmemCols>(tmem_base);
+    else
+      tmem_dealloc<kTmemCols>(tmem_base);
   }
+}
+
+// Host launcher: persistent grid of at most one CTA per SM (pairs when CLUSTER == 2).
+template <int BN, int PASSES, int STAGES, int CLUSTER, class Epi>
+inline cudaError_t launch_tc_gemm(const CUtensorMap& ta, const CUtensorMap& talo,
+                                  const CUtensorMap& tb, const CUtensorMap& tblo, int K,
+                                  TileSched sched, int a_batch_rows, int b_batch_rows,
+                                  const Epi& epi, cudaStream_t stream, int sms) {
+  auto kern = tc_gemm_kernel<BN, PASSES, STAGES, CLUSTER, Epi>;
+  constexpr int smem = gemm_smem_bytes<BN, PASSES, STAGES, CLUSTER>();
+  static_assert(smem <= 232448, "GEMM smem budget exceeded");
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  sched.cluster = CLUSTER;
+  const long units_m = (sched.num_m + CLUSTER - 1) / CLUSTER;
+  const long total = units_m * sched.num_n * sched.num_b;
+  const long max_units = sms / CLUSTER;
+  const int grid = (int)((total < max_units ? total : max_units) * CLUSTER);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kGemmThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CLUSTER;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, talo, tb, tblo, K, sched, a_batch_rows, b_batch_rows,
+                            epi);
 }
 
 }  // namespace astra

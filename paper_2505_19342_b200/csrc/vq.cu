@@ -255,22 +255,53 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
   // records / norms are indexed by token (gathered split) or by source row (pre-split stack)
   const int rr = rec_by_row ? rows[row] : row;
   const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
+  // one round of independent loads: lane c holds chunk record c (nchunk <= 32 for K <= 2048;
+  // larger codebooks loop)
+  const float xn = w.x_norm[(size_t)g * Mrec + rr];
+  const float cmax = cb.c_norm_max[g];
   float best = INFINITY;
-  for (int c = lane; c < nchunk; c += 32) best = fminf(best, w.rec_best[rec0 + c]);
-  for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
-  const float thr = best + 2.0f * score_delta(w.x_norm[(size_t)g * Mrec + rr], cb.c_norm_max[g]);
   int n = 0, only = 0x7FFFFFFF;
   int overflow = 0;
-  for (int c = lane; c < nchunk; c += 32) {
-    if (w.rec_best[rec0 + c] > thr) continue;
-    const int cnt = w.rec_cnt[rec0 + c];
-    if (cnt > kVqCap) overflow = 1;
-    const int m = cnt < kVqCap ? cnt : kVqCap;
-    for (int i = 0; i < m; ++i)
-      if (w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
-        ++n;
-        only = min(only, w.rec_idx[(rec0 + c) * kVqCap + i]);
+  float thr = 0.f;
+  if (nchunk <= 32) {
+    float rb = INFINITY, sc[kVqCap];
+    int rc = 0, ix[kVqCap];
+    if (lane < nchunk) {
+      rb = w.rec_best[rec0 + lane];
+      rc = w.rec_cnt[rec0 + lane];
+#pragma unroll
+      for (int i = 0; i < kVqCap; ++i) {
+        sc[i] = w.rec_score[(rec0 + lane) * kVqCap + i];
+        ix[i] = w.rec_idx[(rec0 + lane) * kVqCap + i];
       }
+    }
+    best = rb;
+    for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    thr = best + 2.0f * score_delta(xn, cmax);
+    if (lane < nchunk && rb <= thr) {
+      if (rc > kVqCap) overflow = 1;
+#pragma unroll
+      for (int i = 0; i < kVqCap; ++i)
+        if (i < rc && sc[i] <= thr) {
+          ++n;
+          only = min(only, ix[i]);
+        }
+    }
+  } else {
+    for (int c = lane; c < nchunk; c += 32) best = fminf(best, w.rec_best[rec0 + c]);
+    for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    thr = best + 2.0f * score_delta(xn, cmax);
+    for (int c = lane; c < nchunk; c += 32) {
+      if (w.rec_best[rec0 + c] > thr) continue;
+      const int cnt = w.rec_cnt[rec0 + c];
+      if (cnt > kVqCap) overflow = 1;
+      const int m = cnt < kVqCap ? cnt : kVqCap;
+      for (int i = 0; i < m; ++i)
+        if (w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
+          ++n;
+          only = min(only, w.rec_idx[(rec0 + c) * kVqCap + i]);
+        }
+    }
   }
   for (int o = 16; o; o >>= 1) {
     n += __shfl_xor_sync(0xffffffffu, n, o);
@@ -429,25 +460,21 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
   if ((st = make_tmap_2d(&talo, a_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * Mg, gdp,
                          lda, kBM, kBK, true)))
     return st;
+  const int cluster = (Mg > kBM) ? 2 : 1;  // CTA pairs split the codebook tile (cta_group::2)
   if ((st = make_tmap_2d(&tb, cb.c_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
-                         gdp, kVqBN, kBK, true)))
+                         gdp, kVqBN / cluster, kBK, true)))
     return st;
   if ((st = make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
-                         gdp, kVqBN, kBK, true)))
+                         gdp, kVqBN / cluster, kBK, true)))
     return st;
   VqEpilogue epi{Mg, K, nchunk, cb.c_sq, cb.c_norm_max, w};
-  auto kern = tc_gemm_kernel<kVqBN, 3, 2, VqEpilogue>;
-  constexpr int smem = gemm_smem_bytes<kVqBN, 3, 2>();
-  static bool configured = false;
-  if (!configured) {
-    ASTRA_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
-  TileSched sched{(Mg + kBM - 1) / kBM, ntile, G};
-  const int tiles = sched.num_m * sched.num_n * sched.num_b;
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kGemmThreads, smem, s>>>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi);
-  ASTRA_CUDA_CHECK(cudaGetLastError());
+  TileSched sched{(Mg + kBM - 1) / kBM, ntile, G, 1};
+  const cudaError_t e =
+      cluster == 2 ? launch_tc_gemm<kVqBN, 3, 3, 2>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi, s,
+                                                    num_sms())
+                   : launch_tc_gemm<kVqBN, 3, 2, 1>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi, s,
+                                                    num_sms());
+  ASTRA_CUDA_CHECK(e);
   const int items = G * M;
   vq_finalize_kernel<<<(items + 7) / 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                       stats, Mg, rec_by_row);
