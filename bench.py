@@ -45,7 +45,7 @@ def _peaks():
         d = json.loads(p.read_text())
         return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d["bf16_tflops_sustained"],
                     src="measured")
-    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1590.0, src="fallback (B200_PROFILING.md)")
 
 
 class Clocks:
@@ -63,11 +63,11 @@ class Clocks:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
-        time.sleep(0.3)
+        time.sleep(0.05)
         return self
 
     def __exit__(self, *a):
@@ -191,6 +191,17 @@ def _kernel_work(rt):
     }
 
 
+def _ncu_traffic(op):
+    """DRAM bytes (read + write) per launch of `op` from the newest committed ncu --set full
+    capture (profiles/traffic_rNN.json); None if that op was not captured."""
+    files = sorted((ROOT / "profiles").glob("traffic_r*.json"))
+    if not files:
+        return None
+    ops = json.loads(files[-1].read_text())["ops"]
+    e = ops.get(op) or ops.get(op + "_gemm")
+    return None if e is None else e["dram_bytes"]
+
+
 def _profile(rt, steps=3):
     import torch
     rt.profile = {}
@@ -209,7 +220,7 @@ def _profile(rt, steps=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fast", choices=["fast", "parity"])
@@ -264,13 +275,11 @@ def main():
             torch.cuda.synchronize()
             rt.graph = None
             graphed = False
-        for _ in range(args.warmup):
-            rt.run()
-        torch.cuda.synchronize()
-        barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clocks = Clocks(local_rank)
-        with clocks:
+        with clocks:   # sampler starts before the warm-up so every sample is taken under load
+            for _ in range(args.warmup):
+                rt.run()
             torch.cuda.synchronize()
             barrier()
             s.record()
@@ -325,16 +334,17 @@ def main():
         kernels[name] = entry
     # dominant kernel = largest share
     dom = max((n for n in kernels if n in work), key=lambda n: kernels[n]["share"])
+    traffic = _ncu_traffic(dom)
     dk = kernels[dom]
     w = work[dom]
     if w["flops"]:
         roof = {"kernel": dom, "bound": "tensor", "achieved": dk["achieved_tflops"],
-                "peak": dk["peak_tflops"], "unit": "TFLOP/s", "frac": dk["frac"], "traffic": None,
+                "peak": dk["peak_tflops"], "unit": "TFLOP/s", "frac": dk["frac"], "traffic": traffic,
                 "peak_source": f"{peaks['src']} bf16 sustained (kernel timed inside the step)",
                 "per_launch": f"{w['flops'] / 1e9:.2f} GFLOP algorithmic"}
     else:
         roof = {"kernel": dom, "bound": "hbm", "achieved": dk["achieved_gbs"], "peak": peaks["hbm"],
-                "unit": "GB/s", "frac": round(dk["achieved_gbs"] / peaks["hbm"], 3), "traffic": None,
+                "unit": "GB/s", "frac": round(dk["achieved_gbs"] / peaks["hbm"], 3), "traffic": traffic,
                 "peak_source": f"{peaks['src']} HBM copy"}
     vq = kernels.get("vq_encode", {})
 
