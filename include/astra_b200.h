@@ -190,7 +190,7 @@ int astra_attention(const void* q, int ldq, const void* k_local, const void* v_l
                     const int32_t* key_src, const int32_t* key_pos, const int32_t* segs,
                     int num_segs, int max_nq, int heads, int head_dim, int causal, int in_bf16,
                     float scale, float* out_f32, void* out_hi, void* out_lo, int ld_out,
-                    void* stream);
+                    int q_rows, int local_rows, int remote_rows, void* stream);
 
 /* Dense-mask form for the operator API (attention.multihead_attention,
  * attention.py:50-73): q [R, D], k/v [C, D] fp32, mask uint8 [R, C] (nonzero =
@@ -202,6 +202,11 @@ int astra_attention_masked(const float* q, const float* k, const float* v, int R
 /* Route astra_attention to the fp32 SIMT kernel even when the tcgen05 bf16
  * kernel applies (test / A-B hook). */
 int astra_attention_force_simt(int enable);
+/* Test hook: tcgen05 variant — 0 persistent warp-specialised (default), 1 one CTA per tile. */
+int astra_attention_variant(int variant);
+/* Debug hook: CTA 0 of the persistent kernel writes per-unit globaltimer stamps
+ * (int64 [64][8]) to buf; NULL disables. */
+int astra_attention_trace(void* buf);
 
 #ifdef __cplusplus
 }

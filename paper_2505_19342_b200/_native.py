@@ -46,8 +46,10 @@ SIGNATURES: dict[str, list] = {
     "astra_key_map": [_vp, _c_int, _vp, _vp, _vp],
     "astra_attention": [_vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int,
                         _c_int, _c_int, _c_int, _c_int, _c_int, ctypes.c_float, _vp, _vp, _vp,
-                        _c_int, _vp],
+                        _c_int, _c_int, _c_int, _c_int, _vp],
     "astra_attention_force_simt": [_c_int],
+    "astra_attention_variant": [_c_int],
+    "astra_attention_trace": [_vp],
     "astra_gather_kv": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _c_int,
                         _vp, _c_int, _vp],
     "astra_append_kv": [_vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp],

@@ -14,6 +14,7 @@
 //
 // v1 is an fp32 SIMT flash-style kernel (online softmax over 64-key tiles, 64x64 fp32 K/V tiles
 // in padded shared memory).  It is exact enough for the fp32 parity mode and general in T.
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <vector>
@@ -179,41 +180,41 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
 }
 
 // ----------------------------------------------------------------------------------------
-// tcgen05 flash attention (bf16 fast path, head_dim 64).  One CTA (4 warps) per
-// (segment, head, 128-query tile); keys stream in chunks of 128:
-//   S = Q K^T on the tensor core (M=128, N=128, K=64) into TMEM,
-//   softmax in registers (thread = query row, tcgen05.ld of its TMEM lane),
-//   P (bf16) written to shared memory in the UMMA K-major SW128 layout,
-//   O_chunk = P V on the tensor core (M=128, N=64, K=128; V used MN-major as stored),
-//   online-softmax rescale of the running output in registers.
-// K/V rows are gathered with cp.async through key_src, which fuses the VQ decode
-// (codebook K/V table rows) into the tile load.
-constexpr int kTQ = 128, kTK = 128;
+// tcgen05 attention (bf16 fast path, head_dim 64).  One CTA (8 warps) per
+// (segment, head, 128-query tile); keys stream in chunks of up to 256, so one chunk covers
+// a whole ViT-B segment (197 keys) and its softmax needs no rescaling:
+//   S = Q K^T        UMMA M=128, N=round16(keys in chunk), K=64      -> TMEM cols [0, 256)
+//   softmax          thread = query row (its TMEM lane); the two warps of a lane quarter
+//                    split the key columns and exchange row max / row sum through smem
+//   P (bf16)         stored back into TMEM over the S columns it was computed from
+//                    (keys 0-127 -> cols 0-63, keys 128-255 -> cols 128-191)
+//   O = P V          UMMA with A read from TMEM, V used MN-major as gathered -> cols [64,128)
+// S, P and O share 256 TMEM columns and ~84 KB of smem: two CTAs (16 warps) per SM.
+// Segments with more than 256 keys take further chunks with the online-softmax rescale of
+// the 32 output columns each thread keeps in registers.
+// K/V rows are gathered with cp.async through key_src, which fuses the VQ decode (codebook
+// K/V table rows) into the tile load.
+constexpr int kTQ = 128, kTKC = 256, kTcThreads = 256;
 static bool g_force_simt_attention = false;  // test hook (astra_attention_force_simt)
-// 16 KB Q + 2 x (16 KB K + 16 KB V) + 32 KB P + 2 x 128 int16 key positions + barrier:
-// 115,264 B, so two CTAs (and their 2 x 256 TMEM columns) share an SM.  The dynamic smem base
-// is 1024-byte aligned (checked at run time), as the SW128 layouts require.
-constexpr int kTcSmem = 16384 + 2 * 32768 + 32768 + 2 * 256 + 64;
+static int g_attention_variant = 0;  // 0 persistent tcgen05, 1 one CTA per tile (astra_attention_variant)
+// Q 16 KB + K 32 KB + V 32 KB + 256 key positions + row max / sum exchange (4 x 128 floats)
+// + barrier and TMEM slot, plus 1 KB to align the base for the SW128 layouts.
+constexpr int kTcSmemUsed = 16384 + 32768 + 32768 + 512 + 2048 + 64;
+constexpr int kTcSmem = kTcSmemUsed + 1024;
 constexpr short kPosNever = 0x7FFF;  // padding key: never visible
 
 __host__ __device__ constexpr uint32_t idesc_bf16_f32_bmn(uint32_t M, uint32_t N) {
   return idesc_bf16_f32(M, N) | (1u << 16);  // B operand MN-major
 }
 
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Issue the cp.async gather of key chunk [kc, kc+128) into (sK, sV) and its positions.
-// Key descriptor of key `key` of the segment (loaded ahead of use: src < 0 marks a remote
-// (codebook-table) row, INT_MIN a padding key).
+// Key descriptor of key `key` of the segment: src < 0 marks a remote (codebook-table) row,
+// INT_MIN a padding key.
 struct KeyRef {
   int src;
   short pos;
@@ -230,11 +231,11 @@ __device__ __forceinline__ KeyRef attn_key_ref(const AttnArgs& a, int k0, int nk
   return r;
 }
 
-// Issue the cp.async gather of one key row per thread (2 x 8 16-byte copies) into the chunk
-// buffers (sK, sV) and record its position; padding keys are zero-filled.
-__device__ __forceinline__ void attn_load_chunk(const AttnArgs& a, KeyRef kr, int hoff,
-                                                uint32_t k_s, uint32_t v_s, uint8_t* sK,
-                                                uint8_t* sV, short* kpos, int tid) {
+// cp.async gather of one key row (its K and V head slices, 2 x 8 16-byte copies) into row
+// `row` of the SW128 chunk buffers; padding keys are zero-filled (P is 0 there, and 0 * a
+// stale NaN would not be).
+__device__ __forceinline__ void attn_load_key(const AttnArgs& a, KeyRef kr, int hoff, int row,
+                                              uint8_t* sK, uint8_t* sV, short* kpos) {
   if (kr.src != INT_MIN) {
     const __nv_bfloat16 *kp, *vp;
     if (kr.src >= 0) {
@@ -246,31 +247,52 @@ __device__ __forceinline__ void attn_load_chunk(const AttnArgs& a, KeyRef kr, in
       vp = reinterpret_cast<const __nv_bfloat16*>(a.v_remote) +
            (size_t)(-(kr.src + 1)) * a.ld_remote + hoff;
     }
+    const uint32_t k_s = smem_u32(sK), v_s = smem_u32(sV);
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      cp_async16(k_s + sw128_offset(tid, c), kp + c * 8);
-      cp_async16(v_s + sw128_offset(tid, c), vp + c * 8);
+      cp_async16(k_s + sw128_offset(row, c), kp + c * 8);
+      cp_async16(v_s + sw128_offset(row, c), vp + c * 8);
     }
   } else {
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      *reinterpret_cast<uint4*>(sK + sw128_offset(tid, c)) = make_uint4(0, 0, 0, 0);
-      *reinterpret_cast<uint4*>(sV + sw128_offset(tid, c)) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(sK + sw128_offset(row, c)) = make_uint4(0, 0, 0, 0);
+      *reinterpret_cast<uint4*>(sV + sw128_offset(row, c)) = make_uint4(0, 0, 0, 0);
     }
   }
-  kpos[tid] = kr.pos;
+  kpos[row] = kr.pos;
 }
 
-__global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = smem_raw;
-  if (smem_u32(sm) & 1023) __trap();      // SW128 tiles need a 1024-byte aligned base
-  uint8_t* sQ = sm;                       // 16 KB
-  uint8_t* sK0 = sm + 16384;              // 2 x 16 KB
-  uint8_t* sV0 = sm + 16384 + 32768;      // 2 x 16 KB
-  uint8_t* sP = sm + 16384 + 65536;       // 32 KB
-  short* sKpos = reinterpret_cast<short*>(sm + 16384 + 98304);   // 2 x 128
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 16384 + 98304 + 512);
+// Visibility bits of the 32 key columns [col0, col0 + 32) of the chunk for a query at
+// position qpos: the chunk tail (non-causal) or key_pos <= qpos (causal; replica keys have
+// position -1, replica / padding queries see everything).
+__device__ __forceinline__ uint32_t attn_vis32(const short* kpos, int col0, int valid, int qpos,
+                                               int causal) {
+  const int left = valid - col0;
+  uint32_t m32 = left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u));
+  if (causal && m32) {
+    uint32_t c32 = 0;
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const short2 kp2 = *reinterpret_cast<const short2*>(kpos + col0 + j);
+      c32 |= (uint32_t)(kp2.x <= qpos) << j;
+      c32 |= (uint32_t)(kp2.y <= qpos) << (j + 1);
+    }
+    m32 &= c32;
+  }
+  return m32;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 2) attention_tc_kernel(AttnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* sQ = sm;                        // 16 KB: 128 query rows x 64 dims, SW128
+  uint8_t* sK = sm + 16384;                // 32 KB: 256 key rows
+  uint8_t* sV = sm + 16384 + 32768;        // 32 KB
+  short* sKpos = reinterpret_cast<short*>(sm + 81920);
+  float* sRed = reinterpret_cast<float*>(sm + 81920 + 512);   // [max | sum][half][128 rows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 81920 + 512 + 2048);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
   const int seg = blockIdx.x, h = blockIdx.y, qt = blockIdx.z;
@@ -278,61 +300,54 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
   const int q0 = sg[0], nq = sg[1], qpos0 = sg[2], ncontent = sg[3], k0 = sg[4], nk = sg[5];
   if (qt * kTQ >= nq) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
   const int hoff = h * 64;
-  const __nv_bfloat16* Q = reinterpret_cast<const __nv_bfloat16*>(a.q);
 
   if (warp == 0) tmem_alloc<256>(tslot);
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_barrier_init();
   }
-  const uint32_t q_s = smem_u32(sQ), p_s = smem_u32(sP);
-  // key descriptors of the first two chunks: loads issued now, consumed after the Q copies
-  const KeyRef kr0 = attn_key_ref(a, k0, nk, tid);
-  const KeyRef kr1 = attn_key_ref(a, k0, nk, kTK + tid);
-  // prologue: group 0 = Q + key chunk 0, group 1 = key chunk 1
+  // Q tile: thread -> row tid/2, four of its eight 16-byte chunks
   {
-    const int qr = qt * kTQ + tid;  // one query row per thread
+    const int row = tid >> 1, c0 = (tid & 1) * 4, qr = qt * kTQ + row;
+    const uint32_t q_s = smem_u32(sQ);
     if (qr < nq) {
-      const __nv_bfloat16* qp = Q + (size_t)(q0 + qr) * a.ldq + hoff;
+      const __nv_bfloat16* qp =
+          reinterpret_cast<const __nv_bfloat16*>(a.q) + (size_t)(q0 + qr) * a.ldq + hoff;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) cp_async16(q_s + sw128_offset(tid, c), qp + c * 8);
+      for (int c = 0; c < 4; ++c) cp_async16(q_s + sw128_offset(row, c0 + c), qp + (c0 + c) * 8);
     } else {
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<uint4*>(sQ + sw128_offset(tid, c)) = make_uint4(0, 0, 0, 0);
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(sQ + sw128_offset(row, c0 + c)) = make_uint4(0, 0, 0, 0);
     }
   }
-  const int nchunks = (nk + kTK - 1) / kTK;
-  attn_load_chunk(a, kr0, hoff, smem_u32(sK0), smem_u32(sV0), sK0, sV0, sKpos, tid);
-  cp_async_commit();
-  if (nchunks > 1)
-    attn_load_chunk(a, kr1, hoff, smem_u32(sK0 + 16384), smem_u32(sV0 + 16384), sK0 + 16384,
-                    sV0 + 16384, sKpos + 128, tid);
-  cp_async_commit();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem, tO = tmem + 128;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
 
-  const int r = warp * 32 + lane;
-  const int qi = qt * kTQ + r;
+  const int row = quarter * 32 + lane;             // this thread's query row = TMEM lane
+  const int qi = qt * kTQ + row;
+  const bool warp_rows = qt * kTQ + quarter * 32 < nq;   // warp-uniform: any valid row
   const int qpos = qi < ncontent ? qpos0 + qi : 0x7FFE;  // replica / pad queries see all keys
-  const float sl2 = a.scale * 1.4426950408889634f;  // exp(x) = exp2(x * log2 e)
-  float m = -INFINITY, l = 0.f;
-  float o[64];
+  const float sl2 = a.scale * 1.4426950408889634f;       // exp(x) = exp2(x * log2 e)
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  float m_run = -INFINITY, l_half = 0.f;
+  float o[32];
 #pragma unroll
-  for (int d = 0; d < 64; ++d) o[d] = 0.f;
+  for (int d = 0; d < 32; ++d) o[d] = 0.f;
+  tc_fence_before();
+  __syncthreads();   // TMEM address and barrier init visible to all
+  tc_fence_after();
+  const uint32_t tmem = *tslot, tS = tmem, tO = tmem + 64;
   uint32_t phase = 0;
 
+  const int nchunks = (nk + kTKC - 1) / kTKC;
   for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1, kc = c * kTK;
-    uint8_t* sK = sK0 + buf * 16384;
-    uint8_t* sV = sV0 + buf * 16384;
-    const short* kpos = sKpos + buf * 128;
-    cp_async_wait_group<1>();   // this chunk's group has landed (the next may be in flight)
+    const int kc = c * kTKC;
+    const int valid = min(kTKC, nk - kc);
+    const int ncols = (valid + 15) & ~15;
+    if (tid < ncols) attn_load_key(a, attn_key_ref(a, k0, nk, kc + tid), hoff, tid, sK, sV, sKpos);
+    cp_async_commit();
+    cp_async_wait_group<0>();
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -340,130 +355,105 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
     if (tid == 0) {
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_f16(tS, sdesc_kmajor_sw128(q_s + kk * 32), sdesc_kmajor_sw128(smem_u32(sK) + kk * 32),
-                 idesc_bf16_f32(128, 128), kk > 0 ? 1u : 0u);
-      umma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-
-    // ---- softmax of row r over this chunk, branch-free: a 32-bit visibility mask per
-    // 32-column group (non-causal: only the chunk tail; causal: key_pos <= query position,
-    // replica keys have position -1) turns masked scores into -inf, so max and exp2 need no
-    // control flow and masked weights come out exactly 0.
-    const int valid = min(kTK, nk - kc);
-    uint32_t vm[4];
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      const int left = valid - cc * 32;
-      uint32_t m32 = left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u));
-      if (a.causal && m32) {
-        uint32_t c32 = 0;
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const short2 kp2 = *reinterpret_cast<const short2*>(kpos + cc * 32 + j);
-          c32 |= (uint32_t)(kp2.x <= qpos) << j;
-          c32 |= (uint32_t)(kp2.y <= qpos) << (j + 1);
-        }
-        m32 &= c32;
-      }
-      vm[cc] = m32;
-    }
-    const int ngroups = (valid + 31) >> 5;
-    float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      if (cc < ngroups) {
-        uint32_t rr[32];
-        tmem_ld32(tS + lane_off + cc * 32, rr);
-        tmem_ld_wait();
-        const uint32_t m32 = vm[cc];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float x = ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY;
-          mx[j & 3] = fmaxf(mx[j & 3], x);
-        }
-      }
-    }
-    const float cmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-    const float mnew = fmaxf(m, cmax * sl2);
-    const float corr = (m == -INFINITY) ? 0.f : ex2_approx(m - mnew);
-    const float mref = (mnew == -INFINITY) ? 0.f : mnew;  // fully masked so far: all p = 0
-    float ls[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      uint32_t pk[16];
-      if (cc < ngroups) {
-        uint32_t rr[32];
-        tmem_ld32(tS + lane_off + cc * 32, rr);
-        tmem_ld_wait();
-        const uint32_t m32 = vm[cc];
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const float x0 = ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY;
-          const float x1 = ((m32 >> (j + 1)) & 1u) ? __uint_as_float(rr[j + 1]) : -INFINITY;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(ex2_approx(fmaf(x0, sl2, -mref)),
-                                                    ex2_approx(fmaf(x1, sl2, -mref)));
-          // sum what the tensor core multiplies (the bf16-rounded probabilities)
-          ls[(j >> 1) & 3] += __low2float(b2) + __high2float(b2);
-          pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = 0u;
-      }
-      const int col0 = cc * 32;
-      uint8_t* blk = sP + (col0 >> 6) * 16384;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int chunk = ((col0 & 63) >> 3) + q;
-        *reinterpret_cast<uint4*>(blk + sw128_offset(r, chunk)) =
-            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-      }
-    }
-    l = l * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
-    m = mnew;
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (tid == 0) {
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        umma_f16(tO, sdesc_kmajor_sw128(p_s + (kk >> 2) * 16384 + (kk & 3) * 32),
-                 sdesc_mnmajor_sw128(smem_u32(sV) + kk * 2048, 8192), idesc_bf16_f32_bmn(128, 64),
+        umma_f16(tS, sdesc_kmajor_sw128(smem_u32(sQ) + kk * 32),
+                 sdesc_kmajor_sw128(smem_u32(sK) + kk * 32), idesc_bf16_f32(128, ncols),
                  kk > 0 ? 1u : 0u);
       umma_commit(bar);
     }
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    {
-      uint32_t r0[32], r1[32];
-      tmem_ld32(tO + lane_off, r0);
-      tmem_ld32(tO + lane_off + 32, r1);
-      tmem_ld_wait();
+
+    // ---- pass 1: row max over this warp's half of the columns (masked scores -> -inf)
+    float mx = -INFINITY;
+    if (warp_rows) {
 #pragma unroll
-      for (int d = 0; d < 32; ++d) {
-        o[d] = fmaf(o[d], corr, __uint_as_float(r0[d]));
-        o[32 + d] = fmaf(o[32 + d], corr, __uint_as_float(r1[d]));
+      for (int gg = 0; gg < 4; ++gg) {
+        const int g = half * 4 + gg;
+        if (g * 32 < valid) {
+          uint32_t rr[32];
+          tmem_ld32(tS + lane_off + g * 32, rr);
+          const uint32_t m32 = attn_vis32(sKpos, g * 32, valid, qpos, a.causal);
+          tmem_ld_wait();
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            m4[j & 3] = fmaxf(m4[j & 3], ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY);
+          mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+        }
       }
     }
+    sRed[half * 128 + row] = mx;
+    __syncthreads();
+    const float cmax = fmaxf(sRed[row], sRed[128 + row]);
+    const float mnew = fmaxf(m_run, cmax * sl2);
+    const float corr = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - mnew);
+    const float mref = (mnew == -INFINITY) ? 0.f : mnew;  // fully masked so far: all p = 0
+
+    // ---- pass 2: p = exp2(s * scale * log2e - m) as bf16, summed as rounded, stored into TMEM
+    float ls[4] = {0.f, 0.f, 0.f, 0.f};
+    if (warp_rows) {
+#pragma unroll
+      for (int gg = 0; gg < 4; ++gg) {
+        const int g = half * 4 + gg;
+        if (g * 32 < valid) {
+          uint32_t rr[32], pk[16];
+          tmem_ld32(tS + lane_off + g * 32, rr);
+          const uint32_t m32 = attn_vis32(sKpos, g * 32, valid, qpos, a.causal);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float x0 = ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY;
+            const float x1 = ((m32 >> (j + 1)) & 1u) ? __uint_as_float(rr[j + 1]) : -INFINITY;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(ex2_approx(fmaf(x0, sl2, -mref)),
+                                                      ex2_approx(fmaf(x1, sl2, -mref)));
+            ls[(j >> 1) & 3] += __low2float(b2) + __high2float(b2);
+            pk[j >> 1] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          // keys 0-127 -> P cols 0-63, keys 128-255 -> P cols 128-191: every column written
+          // here was already read by this thread (same or an earlier group)
+          const int pcol = g < 4 ? g * 16 : 128 + (g - 4) * 16;
+          tmem_st16(tS + lane_off + pcol, pk);
+        }
+      }
+      tmem_st_wait();
+    }
+    l_half = l_half * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
+    m_run = mnew;
     tc_fence_before();
-    __syncthreads();   // buffers of this chunk are free
-    if (c + 2 < nchunks)
-      attn_load_chunk(a, attn_key_ref(a, k0, nk, (c + 2) * kTK + tid), hoff, smem_u32(sK),
-                      smem_u32(sV), sK, sV, sKpos + buf * 128, tid);
-    cp_async_commit();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      const int ksteps = ncols >> 4;
+      for (int kk = 0; kk < ksteps; ++kk) {
+        const uint32_t acol = kk < 8 ? kk * 8 : 128 + (kk - 8) * 8;
+        umma_f16_ts(tO, tS + acol, sdesc_mnmajor_sw128(smem_u32(sV) + kk * 2048, 8192),
+                    idesc_bf16_f32_bmn(128, 64), kk > 0 ? 1u : 0u);
+      }
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    if (warp_rows) {
+      uint32_t r0[32];
+      tmem_ld32(tO + lane_off + half * 32, r0);
+      tmem_ld_wait();
+#pragma unroll
+      for (int d = 0; d < 32; ++d) o[d] = fmaf(o[d], corr, __uint_as_float(r0[d]));
+    }
+    tc_fence_before();
+    __syncthreads();   // K/V buffers and TMEM columns are free for the next chunk
   }
 
+  sRed[256 + half * 128 + row] = l_half;
+  __syncthreads();
   if (qi < nq) {
-    const float inv = 1.0f / l;
-    const size_t ob = (size_t)(q0 + qi) * a.ld_out + hoff;
+    const float inv = 1.0f / (sRed[256 + row] + sRed[384 + row]);
+    const size_t ob = (size_t)(q0 + qi) * a.ld_out + hoff + half * 32;
     if (a.out_hi) {
 #pragma unroll
-      for (int d = 0; d < 64; d += 8) {
+      for (int d = 0; d < 32; d += 8) {
         uint32_t w[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -475,14 +465,492 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs a) {
     }
     if (a.out_f32) {
 #pragma unroll
-      for (int d = 0; d < 64; ++d) a.out_f32[ob + d] = o[d] * inv;
+      for (int d = 0; d < 32; ++d) a.out_f32[ob + d] = o[d] * inv;
     }
   }
-  tc_fence_before();
-  __syncthreads();
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<256>(tmem);
+  }
+}
+
+// ----------------------------------------------------------------------------------------
+// Persistent form of the same computation (the default tcgen05 path): one CTA per SM runs TWO
+// independent attention pipelines side by side, so one's softmax hides the other's MMA and
+// gather latencies.  Pipeline w (w = 0, 1) owns smem stage w, TMEM slot w (256 columns) and
+// the items t = blockIdx.x + (2k + w) * gridDim.x — (segment, head, 128-query tile) — taken
+// 256 keys ("chunk") at a time:
+//   warps 4w..4w+3   softmax: thread = query row = TMEM lane, all key columns of its row
+//                    (no cross-warp exchange): pass 1 row max, pass 2 P = exp2(...) as bf16
+//                    written back into TMEM over the S columns it was computed from, then
+//                    O(chunk) = P V read back into registers with the online-softmax rescale;
+//                    the item's last chunk normalises and stores
+//   warp 8 + w       producer: TMA gather4 of 4 rows per instruction (SW128 applied by smem
+//                    address) — Q rows clamped into the segment, K/V rows through key_src
+//                    (local rows of the projection buffer or codebook-table rows: the fused
+//                    VQ decode); per-thread cp.async would top out at the SM's outstanding-
+//                    miss limit (~16 KB in flight), the TMA engine does not
+//   warp 10 + w      MMA issuer (one thread): S = Q K^T into the slot, O = P V with A = P
+//                    read from TMEM, into columns [128, 192) of the slot
+constexpr int kPThreads = 384;
+constexpr int kPStageBytes = 16384 + 32768 + 32768;     // Q, K, V of one chunk
+constexpr int kPSmemUsed = 2 * kPStageBytes + 2 * 2 * 256 * 4 + 512 + 384 * 32 + 2 * 16384;
+constexpr int kPSmem = kPSmemUsed + 1024;
+
+// Debug timeline (astra_attention_trace): CTA 0 records globaltimer stamps per chunk.
+__device__ long long* g_attn_trace = nullptr;
+__device__ __forceinline__ void p_trace(long long* tr, int slot, uint32_t u) {
+  if (tr != nullptr && u < 32) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[u * 16 + slot] = t;
+  }
+}
+
+struct PBars {   // per pipeline
+  uint64_t qk_full, v_full, qk_empty, v_empty, s_full, p_full, o_full, t_empty, kp_full[2];
+};
+struct PMaps {
+  CUtensorMap q;             // box {64, 128}: a query tile
+  CUtensorMap kl, vl, kr, vr;   // box {64, 1}: gather4 / single rows (local, codebook table)
+  CUtensorMap kl16, vl16;    // box {64, 16}: runs of consecutive local keys
+};
+
+// Item table: at kernel start the CTA decodes its items t = blockIdx.x + i * gridDim.x —
+// (segment, head, 128-query tile) with the q-tile fastest (concurrent CTAs share a segment's
+// K/V in L2) — into shared memory, so the roles' per-item bookkeeping never waits on a global
+// load.  Item i belongs to pipeline i % 2; items past the table capacity are decoded from
+// global memory.
+constexpr int kPItemCap = 384;
+struct PItem {
+  int q0, nq, qpos0, ncontent, k0, nk, h, qt;
+};
+struct PUnit {
+  int q0, nq, qpos0, ncontent, k0, nk, h, qt, kc;
+  bool ok;
+};
+__device__ __forceinline__ PItem p_decode(const AttnArgs& a, int qtiles, int t) {
+  PItem r;
+  r.qt = t % qtiles;
+  r.h = (t / qtiles) % a.heads;
+  const int* sg = a.segs + (t / qtiles / a.heads) * 6;
+  r.q0 = __ldg(sg);
+  r.nq = __ldg(sg + 1);
+  r.qpos0 = __ldg(sg + 2);
+  r.ncontent = __ldg(sg + 3);
+  r.k0 = __ldg(sg + 4);
+  r.nk = __ldg(sg + 5);
+  return r;
+}
+struct PIter {
+  int i, n_items, qtiles;
+  const PItem* table;
+  PUnit cur;
+  __device__ __forceinline__ void next_item(const AttnArgs& a) {
+    cur.ok = false;
+    for (; i < n_items; i += 2) {
+      const PItem e = i < kPItemCap ? table[i] : p_decode(a, qtiles, blockIdx.x + i * gridDim.x);
+      if (e.qt * kTQ < e.nq && e.nk > 0) {
+        cur.q0 = e.q0;
+        cur.nq = e.nq;
+        cur.qpos0 = e.qpos0;
+        cur.ncontent = e.ncontent;
+        cur.k0 = e.k0;
+        cur.nk = e.nk;
+        cur.h = e.h;
+        cur.qt = e.qt;
+        cur.kc = 0;
+        cur.ok = true;
+        i += 2;
+        return;
+      }
+    }
+  }
+  __device__ __forceinline__ void init(const AttnArgs& a, int qt_, int pipe, const PItem* tab,
+                                       int n) {
+    qtiles = qt_;
+    table = tab;
+    n_items = n;
+    i = pipe;
+    next_item(a);
+  }
+  __device__ __forceinline__ void advance(const AttnArgs& a) {
+    if (!cur.ok) return;
+    cur.kc += kTKC;
+    if (cur.kc >= cur.nk) next_item(a);
+  }
+};
+
+// key_src of the 16 key rows 16*lane .. 16*lane+15 of a chunk (lanes 0-15).  Rows past the
+// chunk end (inside its last 16-key MMA step) continue a local run (rows of the next segment,
+// or zero-filled past the buffer) or repeat the last codebook row: finite data that P = 0
+// multiplies away.
+__device__ __forceinline__ void p_fetch_rows(const AttnArgs& a, const PUnit& un, int lane,
+                                             int (&r)[16]) {
+  const int valid = min(kTKC, un.nk - un.kc);
+  const int32_t* ks = a.key_src + un.k0 + un.kc;
+  const int last = __ldg(ks + valid - 1);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int j = 16 * lane + i;
+    r[i] = j < valid ? __ldg(ks + j) : (last >= 0 ? last + (j - valid + 1) : last);
+  }
+}
+
+// Gather this lane's 16 key rows (K or V) into `dst`: one 16-row box when they are a run of
+// consecutive local rows (N = 1: every group), else a TMA gather4 per 4 rows from one source,
+// else single rows.
+template <bool kV>
+__device__ __forceinline__ void p_gather_keys(const PMaps& mp, const PUnit& un, const int (&r)[16],
+                                              uint8_t* dst, uint64_t* bar, int lane) {
+  const int ncols = (min(kTKC, un.nk - un.kc) + 15) & ~15;
+  if (16 * lane >= ncols) return;
+  const int col = un.h * 64;
+  uint8_t* d = dst + lane * 2048;
+  bool run = r[0] >= 0;
+#pragma unroll
+  for (int i = 1; i < 16; ++i) run &= r[i] == r[0] + i;
+  if (run) {
+    tma_load_2d(d, kV ? &mp.vl16 : &mp.kl16, bar, col, r[0], kEvictNormal);
+    return;
+  }
+  const CUtensorMap* ml = kV ? &mp.vl : &mp.kl;
+  const CUtensorMap* mr = kV ? &mp.vr : &mp.kr;
+#pragma unroll
+  for (int qd = 0; qd < 4; ++qd) {
+    const int* q = r + 4 * qd;
+    const bool all_local = (q[0] >= 0) & (q[1] >= 0) & (q[2] >= 0) & (q[3] >= 0);
+    const bool all_remote = (q[0] < 0) & (q[1] < 0) & (q[2] < 0) & (q[3] < 0);
+    if (all_local) {
+      tma_gather4(d + qd * 512, ml, bar, col, q[0], q[1], q[2], q[3]);
+    } else if (all_remote) {
+      tma_gather4(d + qd * 512, mr, bar, col, -(q[0] + 1), -(q[1] + 1), -(q[2] + 1), -(q[3] + 1));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        tma_load_2d(d + qd * 512 + i * 128, q[i] >= 0 ? ml : mr, bar, col,
+                    q[i] >= 0 ? q[i] : -(q[i] + 1), kEvictNormal);
+    }
+  }
+}
+
+// Producer warp of one pipeline: Q + K of chunk n once S(n-1) retired, V once O(n-1) retired.
+template <bool kCausal>
+__device__ __forceinline__ void p_producer(const AttnArgs& a, const PMaps& mp, int qtiles, int pipe,
+                                           const PItem* items, int n_items, uint8_t* st,
+                                           int* kpos2, PBars* b, int lane, long long* trace) {
+  PIter it;
+  it.init(a, qtiles, pipe, items, n_items);
+  for (uint32_t n = 0; it.cur.ok; ++n, it.advance(a)) {
+    const PUnit un = it.cur;
+    const uint32_t ph = n & 1;
+    const int valid = min(kTKC, un.nk - un.kc), ncols = (valid + 15) & ~15;
+    int rows[16];   // this lane's key rows, loaded before the stage wait (latency hidden)
+    if (lane < 16) p_fetch_rows(a, un, lane, rows);
+    int kpv[8];
+    if (kCausal) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int j = lane + 32 * m;
+        kpv[m] = j < valid ? __ldg(a.key_pos + un.k0 + un.kc + j) : 0x7FFFFFFF;
+      }
+    }
+    mbar_wait_spin(&b->qk_empty, ph ^ 1);
+    if (lane == 0) p_trace(trace, 6 + pipe * 8, n);
+    if (kCausal) {
+      // key positions (plain stores + release arrive).  Buffer n%2 was last read by the
+      // softmax of chunk n-2, which ended before S(n-1) (just retired) was issued.
+      int* kp = kpos2 + (n & 1) * 256;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) kp[lane + 32 * m] = kpv[m];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&b->kp_full[n & 1]);
+    }
+    if (lane == 0) mbar_arrive_expect_tx(&b->qk_full, (128 + ncols) * 128);
+    __syncwarp();
+    // Q: one 128-row box (rows past nq belong to the next segment or are zero-filled past the
+    // buffer; they are computed and never stored)
+    if (lane == 16) tma_load_2d(st, &mp.q, &b->qk_full, un.h * 64, un.q0 + un.qt * kTQ, kEvictNormal);
+    if (lane < 16) p_gather_keys<false>(mp, un, rows, st + 16384, &b->qk_full, lane);
+    if (lane == 0) p_trace(trace, 0 + pipe * 8, n);
+    mbar_wait_spin(&b->v_empty, ph ^ 1);
+    if (lane == 0) mbar_arrive_expect_tx(&b->v_full, ncols * 128);
+    __syncwarp();
+    if (lane < 16) p_gather_keys<true>(mp, un, rows, st + 16384 + 32768, &b->v_full, lane);
+  }
+}
+
+// MMA issuer of one pipeline (one thread): S(n) = Q K^T, then O(n) = P V once P is in TMEM.
+__device__ __forceinline__ void p_mma(const AttnArgs& a, int qtiles, int pipe, const PItem* items,
+                                      int n_items, uint8_t* st, uint32_t tS, PBars* b,
+                                      long long* trace) {
+  PIter it;
+  it.init(a, qtiles, pipe, items, n_items);
+  const uint32_t q_s = smem_u32(st), k_s = q_s + 16384, v_s = k_s + 32768;
+  for (uint32_t n = 0; it.cur.ok; ++n, it.advance(a)) {
+    const uint32_t ph = n & 1;
+    const int ncols = (min(kTKC, it.cur.nk - it.cur.kc) + 15) & ~15;
+    mbar_wait_spin(&b->t_empty, ph ^ 1);   // O(n-1) read back: the slot is free
+    mbar_wait_spin(&b->qk_full, ph);
+    tc_fence_after();
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      umma_f16(tS, sdesc_kmajor_sw128(q_s + kk * 32), sdesc_kmajor_sw128(k_s + kk * 32),
+               idesc_bf16_f32(128, ncols), kk > 0 ? 1u : 0u);
+    umma_commit(&b->s_full);
+    umma_commit(&b->qk_empty);
+    p_trace(trace, 1 + pipe * 8, n);
+    if (trace) {   // debug: when does S actually complete?
+      mbar_wait_spin(&b->s_full, ph);
+      p_trace(trace, 5 + pipe * 8, n);
+    }
+    mbar_wait_spin(&b->p_full, ph);
+    mbar_wait_spin(&b->v_full, ph);
+    tc_fence_after();
+    for (int kk = 0; kk < (ncols >> 4); ++kk)
+      umma_f16_ts(tS + 128, tS + kk * 8, sdesc_mnmajor_sw128(v_s + kk * 2048, 8192),
+                  idesc_bf16_f32_bmn(128, 64), kk > 0 ? 1u : 0u);
+    umma_commit(&b->o_full);
+    umma_commit(&b->v_empty);
+    p_trace(trace, 2 + pipe * 8, n);
+  }
+}
+
+// Visibility bits of 32 key columns: the chunk tail (`left` keys remain) and, when causal,
+// key_pos <= the query's position.
+template <bool kCausal>
+__device__ __forceinline__ uint32_t p_vis(const int* kpos, int left, int qpos) {
+  uint32_t m32 = left >= 32 ? 0xffffffffu : ((1u << left) - 1u);
+  if (kCausal) {
+    uint32_t c32 = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) c32 |= (uint32_t)(kpos[j] <= qpos) << j;
+    m32 &= c32;
+  }
+  return m32;
+}
+
+// Softmax warpgroup of one pipeline.
+template <bool kCausal>
+__device__ __forceinline__ void p_softmax(const AttnArgs& a, int qtiles, int pipe,
+                                          const PItem* items, int n_items, uint32_t tS,
+                                          const int* kpos2, PBars* b, uint8_t* ostage,
+                                          int quarter, int lane, long long* trace) {
+  const int row = quarter * 32 + lane;
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  const float sl2 = a.scale * 1.4426950408889634f;
+  float o[64];
+#pragma unroll
+  for (int d = 0; d < 64; ++d) o[d] = 0.f;
+  float m_run = -INFINITY, l = 0.f;
+  PIter it;
+  it.init(a, qtiles, pipe, items, n_items);
+  for (uint32_t n = 0; it.cur.ok; ++n, it.advance(a)) {
+    const PUnit un = it.cur;
+    const uint32_t ph = n & 1;
+    const int valid = min(kTKC, un.nk - un.kc);
+    const int qi = un.qt * kTQ + row;
+    const bool warp_rows = un.qt * kTQ + quarter * 32 < un.nq;
+    const int qpos = qi < un.ncontent ? un.qpos0 + qi : 0x7FFE;
+    const int* kpos = kpos2 + (n & 1) * 256;
+    if (un.kc == 0) {
+      m_run = -INFINITY;
+      l = 0.f;
+    }
+    if (quarter == 0 && lane == 0) p_trace(trace, 7 + pipe * 8, n);
+    if (kCausal) mbar_wait_spin(&b->kp_full[n & 1], (n >> 1) & 1);
+    mbar_wait_spin(&b->s_full, ph);
+    tc_fence_after();
+    if (quarter == 0 && lane == 0) p_trace(trace, 3 + pipe * 8, n);
+    float corr = 0.f, mref = 0.f, mnew = m_run;
+    if (warp_rows) {
+      // pass 1: row max (fully visible groups skip the mask selects)
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int g = 0; g * 32 < valid; ++g) {
+        uint32_t rr[32];
+        tmem_ld32(tS + lane_off + g * 32, rr);
+        const int left = valid - g * 32;
+        const uint32_t m32 = p_vis<kCausal>(kpos + g * 32, left, qpos);
+        tmem_ld_wait();
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (!kCausal && left >= 32) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(rr[j]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            m4[j & 3] = fmaxf(m4[j & 3], ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY);
+        }
+        mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+      }
+      mnew = fmaxf(m_run, mx * sl2);
+      corr = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - mnew);
+      mref = (mnew == -INFINITY) ? 0.f : mnew;
+      // pass 2: P = exp2(s*scale*log2e - m) in bf16, group g packed into TMEM cols 16g..16g+15
+      // (already read by this thread in group g/2); packed fp32 pairs for the affine step and
+      // the row sum (of the unrounded probabilities)
+      const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-mref, -mref);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                       make_float2(0.f, 0.f)};
+#pragma unroll 1
+      for (int g = 0; g * 32 < valid; ++g) {
+        uint32_t rr[32], pk[16];
+        tmem_ld32(tS + lane_off + g * 32, rr);
+        const int left = valid - g * 32;
+        const uint32_t m32 = p_vis<kCausal>(kpos + g * 32, left, qpos);
+        tmem_ld_wait();
+        if (!kCausal && left >= 32) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float2 t = ffma2(make_float2(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])),
+                                   sl2x2, nm2);
+            const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+            pk[j >> 1] = pack_bf16x2(e.x, e.y);
+            acc[(j >> 1) & 3] = fadd2(acc[(j >> 1) & 3], e);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float x0 = ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY;
+            const float x1 = ((m32 >> (j + 1)) & 1u) ? __uint_as_float(rr[j + 1]) : -INFINITY;
+            const float2 t = ffma2(make_float2(x0, x1), sl2x2, nm2);
+            const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+            pk[j >> 1] = pack_bf16x2(e.x, e.y);
+            acc[(j >> 1) & 3] = fadd2(acc[(j >> 1) & 3], e);
+          }
+        }
+        tmem_st16(tS + lane_off + g * 16, pk);
+      }
+      tmem_st_wait();
+      const float2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+      l = l * corr + ((s01.x + s01.y) + (s23.x + s23.y));
+    }
+    m_run = mnew;
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&b->p_full);
+    mbar_wait_spin(&b->o_full, ph);
+    tc_fence_after();
+    if (warp_rows) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t r0[32];
+        tmem_ld32(tS + 128 + lane_off + hh * 32, r0);
+        tmem_ld_wait();
+        // corr = 0 on an item's first chunk clears what the previous item left in o
+#pragma unroll
+        for (int d = 0; d < 32; ++d) o[hh * 32 + d] = fmaf(o[hh * 32 + d], corr, __uint_as_float(r0[d]));
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&b->t_empty);
+    if (un.kc + kTKC >= un.nk && warp_rows) {
+      const float inv = 1.0f / l;
+      if (a.out_hi) {
+        // stage the warp's 32 output rows (128 B each, 16-byte chunks XOR-swizzled by row) and
+        // write them back as whole rows: 4 rows per warp instruction instead of 32 scattered
+        // 16-byte pieces
+        uint8_t* stg = ostage + quarter * 4096;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4 w;
+          w.x = pack_bf16x2(o[8 * c] * inv, o[8 * c + 1] * inv);
+          w.y = pack_bf16x2(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
+          w.z = pack_bf16x2(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
+          w.w = pack_bf16x2(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+          *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) = w;
+        }
+        __syncwarp();
+        const int rbase = un.qt * kTQ + quarter * 32;
+#pragma unroll
+        for (int it2 = 0; it2 < 8; ++it2) {
+          const int r = 4 * it2 + (lane >> 3), c = lane & 7;
+          if (rbase + r < un.nq)
+            *reinterpret_cast<uint4*>(a.out_hi + (size_t)(un.q0 + rbase + r) * a.ld_out + un.h * 64 + 8 * c) =
+                *reinterpret_cast<const uint4*>(stg + r * 128 + ((c ^ (r & 7)) << 4));
+        }
+        __syncwarp();
+      }
+      if (a.out_f32 && qi < un.nq) {
+        const size_t ob = (size_t)(un.q0 + qi) * a.ld_out + un.h * 64;
+#pragma unroll
+        for (int d = 0; d < 64; ++d) a.out_f32[ob + d] = o[d] * inv;
+      }
+    }
+    if (quarter == 0 && lane == 0) p_trace(trace, 4 + pipe * 8, n);
+  }
+}
+
+template <bool kCausal>
+__global__ void __launch_bounds__(kPThreads, 1)
+    attention_tcp_kernel(AttnArgs a, const __grid_constant__ PMaps mp, int qtiles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  int* sKpos = reinterpret_cast<int*>(sm + 2 * kPStageBytes);          // [pipe][2][256]
+  PBars* bars = reinterpret_cast<PBars*>(sKpos + 2 * 2 * 256);         // [pipe]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  PItem* items = reinterpret_cast<PItem*>(sm + 2 * kPStageBytes + 2 * 2 * 256 * 4 + 512);
+  uint8_t* ostage = reinterpret_cast<uint8_t*>(items + kPItemCap);   // [pipe][4 warps][4 KB]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  long long* const trace = blockIdx.x == 0 ? g_attn_trace : nullptr;   // debug timeline
+
+  if (tid == 0) {
+    for (int w = 0; w < 2; ++w) {
+      PBars* b = bars + w;
+      mbar_init(&b->qk_full, 1);
+      mbar_init(&b->v_full, 1);
+      mbar_init(&b->qk_empty, 1);
+      mbar_init(&b->v_empty, 1);
+      mbar_init(&b->s_full, 1);
+      mbar_init(&b->p_full, 4);
+      mbar_init(&b->o_full, 1);
+      mbar_init(&b->t_empty, 4);
+      mbar_init(&b->kp_full[0], 1);
+      mbar_init(&b->kp_full[1], 1);
+    }
+    fence_barrier_init();
+  }
+  const int total = a.num_segs * a.heads * qtiles;
+  const int n_items = total > (int)blockIdx.x ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  for (int i = tid; i < min(n_items, kPItemCap); i += kPThreads)
+    items[i] = p_decode(a, qtiles, blockIdx.x + i * gridDim.x);
+  if (warp == 10) tmem_alloc<512>(tslot);
+  if (tid == 256) {
+    tma_prefetch_desc(&mp.q);
+    tma_prefetch_desc(&mp.kl);
+    tma_prefetch_desc(&mp.vl);
+    tma_prefetch_desc(&mp.kr);
+    tma_prefetch_desc(&mp.vr);
+    tma_prefetch_desc(&mp.kl16);
+    tma_prefetch_desc(&mp.vl16);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp < 8) {
+    const int pipe = warp >> 2;
+    p_softmax<kCausal>(a, qtiles, pipe, items, n_items, tmem + pipe * 256, sKpos + pipe * 512,
+                       bars + pipe, ostage + pipe * 16384, warp & 3, lane, trace);
+  } else if (warp < 10) {
+    const int pipe = warp - 8;
+    p_producer<kCausal>(a, mp, qtiles, pipe, items, n_items, sm + pipe * kPStageBytes,
+                        sKpos + pipe * 512, bars + pipe, lane, trace);
+  } else if (lane == 0) {
+    const int pipe = warp - 10;
+    p_mma(a, qtiles, pipe, items, n_items, sm + pipe * kPStageBytes, tmem + pipe * 256,
+          bars + pipe, trace);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 10) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
   }
 }
 
@@ -514,7 +982,8 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
                                int ld_remote, const int32_t* key_src, const int32_t* key_pos,
                                const int32_t* segs, int num_segs, int max_nq, int heads,
                                int head_dim, int causal, int in_bf16, float scale, float* out_f32,
-                               void* out_hi, void* out_lo, int ld_out, void* stream) {
+                               void* out_hi, void* out_lo, int ld_out, int q_rows,
+                               int local_rows, int remote_rows, void* stream) {
   ASTRA_REQUIRE(head_dim == 4 || head_dim == 8 || head_dim == 16 || head_dim == 32 || head_dim == 64 ||
                     head_dim == 128,
                 ASTRA_ERR_SHAPE, "attention: head_dim %d unsupported", head_dim);
@@ -535,10 +1004,38 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
     if (!configured) {
       ASTRA_CUDA_CHECK(cudaFuncSetAttribute(attention_tc_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
+      ASTRA_CUDA_CHECK(cudaFuncSetAttribute(attention_tcp_kernel<false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+      ASTRA_CUDA_CHECK(cudaFuncSetAttribute(attention_tcp_kernel<true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
       configured = true;
     }
-    dim3 tgrid(num_segs, heads, (max_nq + kTQ - 1) / kTQ);
-    attention_tc_kernel<<<tgrid, 128, kTcSmem, st>>>(a);
+    const int qtiles = (max_nq + kTQ - 1) / kTQ;
+    if (g_attention_variant == 0) {
+      const long items = (long)num_segs * heads * qtiles;
+      const int grid = (int)std::min<long>(items, num_sms());
+      // gather maps (SW128, true row extents: boxes running past a buffer are zero-filled)
+      PMaps mp;
+      const auto bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+      const uint64_t qr = std::max(q_rows, 1), lr = std::max(local_rows, 1),
+                     rr = std::max(remote_rows, 1);
+      int rc;
+      if ((rc = make_tmap_2d(&mp.q, q, bf, 2, qr, ldq, ldq, kTQ, 64, true)) ||
+          (rc = make_tmap_2d(&mp.kl, k_local, bf, 2, lr, ld_local, ld_local, 1, 64, true)) ||
+          (rc = make_tmap_2d(&mp.vl, v_local, bf, 2, lr, ld_local, ld_local, 1, 64, true)) ||
+          (rc = make_tmap_2d(&mp.kl16, k_local, bf, 2, lr, ld_local, ld_local, 16, 64, true)) ||
+          (rc = make_tmap_2d(&mp.vl16, v_local, bf, 2, lr, ld_local, ld_local, 16, 64, true)) ||
+          (rc = make_tmap_2d(&mp.kr, k_remote, bf, 2, rr, ld_remote, ld_remote, 1, 64, true)) ||
+          (rc = make_tmap_2d(&mp.vr, v_remote, bf, 2, rr, ld_remote, ld_remote, 1, 64, true)))
+        return rc;
+      if (causal)
+        attention_tcp_kernel<true><<<grid, kPThreads, kPSmem, st>>>(a, mp, qtiles);
+      else
+        attention_tcp_kernel<false><<<grid, kPThreads, kPSmem, st>>>(a, mp, qtiles);
+    } else {
+      dim3 tgrid(num_segs, heads, qtiles);
+      attention_tc_kernel<<<tgrid, kTcThreads, kTcSmem, st>>>(a);
+    }
     ASTRA_CUDA_CHECK(cudaGetLastError());
     return ASTRA_OK;
   }
@@ -554,6 +1051,17 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
   }
   if (rc) return rc;
   ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_attention_trace(void* buf) {
+  long long* p = reinterpret_cast<long long*>(buf);
+  ASTRA_CUDA_CHECK(cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)));
+  return ASTRA_OK;
+}
+
+extern "C" int astra_attention_variant(int variant) {
+  g_attention_variant = variant;
   return ASTRA_OK;
 }
 

@@ -48,12 +48,28 @@ ASTRA_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 ASTRA_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Blocks until the phase with `parity` completes (try_wait spin: the hardware already parks a
+// waiting warp for a short, system-dependent time per probe).
 ASTRA_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// Same, polling with mbarrier.test_wait (never parks the warp): try_wait may suspend a warp
+// for a system-dependent time and wake it late (~0.5 us measured) — too slow for a
+// latency-critical hand-off between warps of a pipeline.
+ASTRA_DEVICE void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(addr),
       "r"(parity)
       : "memory");
@@ -70,6 +86,17 @@ ASTRA_DEVICE void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, i
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
+      : "memory");
+}
+// Gather of four rows (r0..r3, any order) of a 2-D tensor whose box is {cols, 1}: the rows
+// land back to back at smem_dst with the tensor map's swizzle applied by smem address.
+ASTRA_DEVICE void tma_gather4(void* smem_dst, const void* desc, uint64_t* bar, int col, int r0,
+                              int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3)
       : "memory");
 }
 // 3-D tiled load: (inner, mid, outer).
@@ -264,7 +291,58 @@ ASTRA_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 ASTRA_DEVICE void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// 16 registers per thread -> 32 lanes x 16 columns of 32-bit TMEM.
+ASTRA_DEVICE void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+ASTRA_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]: A (M x K, K-major) read from TMEM — row m in lane m, two
+// bf16 K-elements per 32-bit column — B through a shared-memory descriptor.
+ASTRA_DEVICE void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
 // --------------------------------------------------------------- numerics
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two lanes of work per issue slot).
+ASTRA_DEVICE float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+ASTRA_DEVICE float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+ASTRA_DEVICE float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+ASTRA_DEVICE uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 // Split an fp32 value into bf16 hi + bf16 lo (x ~= hi + lo, |x-hi-lo| <= 2^-16 |x|).
 ASTRA_DEVICE void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
   hi = __float2bfloat16_rn(x);
@@ -300,23 +378,21 @@ ASTRA_DEVICE float gelu_erf(float x) {
   return x * (x >= 0.0f ? 1.0f - h : h);
 }
 
-// Same construction with a degree-8 R (max |error| 2.7e-5, relative 2.7e-4 where |gelu| >
-// 1e-2): for the bf16 fast path, whose output rounding (3.9e-3 relative) dominates.
+// bf16-output GELU for the fast path: x * Phi(x) with Phi(x) = 1 / (1 + 2^-v(x)), v an odd
+// degree-5 polynomial fitted (minimax, fp32 evaluation) to log2(Phi / (1 - Phi)) on [-5, 5];
+// the logistic form has no cancellation on either tail.  Max |error| vs the exact erf GELU
+// 2.6e-5 over |x| <= 50 (relative 1.2e-3 where |gelu| > 1e-2, below the bf16 output's half
+// ulp).  10 instructions, two of them MUFU (ex2, rcp) — half the issue slots of the erfc
+// polynomial, which bound the W1 epilogue.
 ASTRA_DEVICE float gelu_erf_bf16(float x) {
-  const float z = fabsf(x) * 0.70710678118654752f;
-  const float e = exp2f(-(z * z) * 1.4426950408889634f);
-  const float u = fminf(z, 4.0f) - 2.0f;
-  float r = 0.00013683406605387587f;
-  r = fmaf(r, u, -0.00043860508011060994f);
-  r = fmaf(r, u, 0.00025942515572788624f);
-  r = fmaf(r, u, -0.0009406567103610213f);
-  r = fmaf(r, u, 0.005955796716703947f);
-  r = fmaf(r, u, -0.01653105315666264f);
-  r = fmaf(r, u, 0.041532531022877815f);
-  r = fmaf(r, u, -0.10645975582795f);
-  r = fmaf(r, u, 0.2554180079701582f);
-  const float h = 0.5f * e * r;
-  return x * (x >= 0.0f ? 1.0f - h : h);
+  const float xc = fminf(fmaxf(x, -5.0f), 5.0f);
+  const float x2 = xc * xc;
+  const float p = fmaf(fmaf(-0.0010147804887581664f, x2, 0.10677938108922315f), x2,
+                       2.3011167090624842f);
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(p * -xc));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return x * r;
 }
 
 }  // namespace astra

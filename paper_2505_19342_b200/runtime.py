@@ -395,7 +395,7 @@ class AstraRuntime:
                      _p(remote, D), ld_r, self.key_src.data_ptr(), self.key_pos.data_ptr(),
                      self.segs.data_ptr(), self.n_segs, self.max_nq, self.H, self.dk,
                      int(self.cfg.causal), int(self.fast), float(np.float32(1.0 / math.sqrt(self.dk))),
-                     None, self.o_hi.data_ptr(), _p(self.o_lo), D, s)
+                     None, self.o_hi.data_ptr(), _p(self.o_lo), D, R, R, remote.shape[0], s)
         # 6. h = stack + attn Wo
         whi, wlo = lay["wo"]
         with self._op("gemm_wo"):
@@ -600,7 +600,8 @@ class AstraRuntime:
                          _p(cache, D), 2 * D, cache.data_ptr(), _p(cache, D), 2 * D,
                          self.dec_key_src.data_ptr(), self.dec_key_pos.data_ptr(),
                          self.dec_segs.data_ptr(), B, 1, self.H, self.dk, 0, int(self.fast),
-                         scale, None, self.dec_o_hi.data_ptr(), _p(self.dec_o_lo), D, s)
+                         scale, None, self.dec_o_hi.data_ptr(), _p(self.dec_o_lo), D, B,
+                         cache.shape[0], cache.shape[0], s)
             self._gemm_rows(lay["wo"], self.dec_o_hi, self.dec_o_lo, residual=X, out_f32=H)
             _native.call("astra_layernorm", H.data_ptr(), B, D, D, lay["ln2_g"].data_ptr(),
                          lay["ln2_b"].data_ptr(), LN_EPS, None, 0, self.dec_ln_hi.data_ptr(),

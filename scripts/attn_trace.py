@@ -1,0 +1,42 @@
+"""Timeline of the persistent attention kernel (CTA 0) on the ViT-B/16 B=64 workload:
+per unit, globaltimer stamps of the loader / MMA / softmax events (debug aid)."""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2505_19342_b200 import _native, cluster, data, model, vq  # noqa: E402
+from paper_2505_19342_b200.runtime import AstraRuntime  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+cfg = model.ModelConfig(layers=1, hidden=768, heads=12, vocab_or_classes=1000, max_tokens=197,
+                        causal=False, codebook_size=1024, groups=1)
+params = model.init_params(cfg, seed=0)
+xs = data.make_classify_batch(768, 196, 64, seed=1)
+rng = np.random.default_rng(0)
+for i, b in enumerate(params.blocks):
+    c = xs.reshape(-1, 768)[rng.choice(64 * 196, 1024, replace=False)]
+    b.codebook = vq.Codebook(layer_id=i, groups=1, centroids=[c])
+rt = AstraRuntime(params, cluster.partition_tokens(196, n), batch=64, precision="fast")
+rt.stage_input(xs)
+rt.forward()
+torch.cuda.synchronize()
+buf = torch.zeros(32 * 16, dtype=torch.int64, device="cuda")
+lib = _native.load()
+lib.astra_attention_trace(buf.data_ptr())
+rt.profile = {}
+rt.forward()
+torch.cuda.synchronize()
+lib.astra_attention_trace(None)
+ms = [s.elapsed_time(e) for s, e in rt.profile["attention"]]
+print("attention ms", ms)
+t = buf.view(32, 16).cpu().numpy().astype(np.int64)
+t0 = t[t > 0].min()
+names = ["0qk", "0S", "0PV", "0sm_st", "0sm_end", "0Sdone", "0pgo", "0top", "1qk", "1S", "1PV", "1sm_st", "1sm_end", "1Sdone", "1pgo", "1top"]
+print("unit " + " ".join(f"{x:>8s}" for x in names))
+for u in range(32):
+    if t[u].max() == 0:
+        break
+    print(f"{u:4d} " + " ".join(f"{(v - t0) / 1000:8.2f}" if v else "       -" for v in t[u]))

@@ -91,13 +91,13 @@ def test_dropin_attention_errors(cuda):
 
 
 SPECS = [[(197, 197, 1)], [(50, 197, 1), (49, 197, 1), (25, 197, 1)], [(130, 300, 0), (7, 7, 0)],
-         [(256, 129, 1)]]
+         [(256, 129, 1)], [(200, 600, 1), (64, 256, 0), (16, 16, 1)], [(1, 257, 1)]]
 
 
 @pytest.mark.parametrize("spec", SPECS)
 @pytest.mark.parametrize("causal", [False, True])
-@pytest.mark.parametrize("force_simt", [False, True])
-def test_attention_kernels_vs_torch(cuda, spec, causal, force_simt):
+@pytest.mark.parametrize("force_simt,variant", [(False, 0), (False, 1), (True, 0)])
+def test_attention_kernels_vs_torch(cuda, spec, causal, force_simt, variant):
     from paper_2505_19342_b200 import _native
     heads, dk = 12, 64
     qkv, table, segs_t, ks, kp, segs = _problem(len(spec) + 7 * causal, spec, heads, dk, causal)
@@ -105,6 +105,7 @@ def test_attention_kernels_vs_torch(cuda, spec, causal, force_simt):
     out = torch.zeros(qkv.shape[0], D, dtype=torch.bfloat16, device="cuda")
     lib = _native.load()
     lib.astra_attention_force_simt(int(force_simt))
+    lib.astra_attention_variant(variant)
     try:
         es = qkv.element_size()
         _native.call("astra_attention", qkv.data_ptr(), 3 * D, qkv.data_ptr() + D * es,
@@ -112,10 +113,12 @@ def test_attention_kernels_vs_torch(cuda, spec, causal, force_simt):
                      table.data_ptr() + D * es, 2 * D, ks.data_ptr(), kp.data_ptr(),
                      segs_t.data_ptr(), len(segs), max(s[1] for s in segs), heads, dk, int(causal),
                      1, float(np.float32(1 / math.sqrt(dk))), None, out.data_ptr(), None, D,
+                     qkv.shape[0], qkv.shape[0], table.shape[0],
                      torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
     finally:
         lib.astra_attention_force_simt(0)
+        lib.astra_attention_variant(0)
     ref = _reference(qkv, table, segs, ks, kp, heads, dk, causal)
     rows = torch.cat([torch.arange(s[0], s[0] + s[1]) for s in segs]).cuda()
     err = (out.float()[rows] - ref[rows]).abs().max().item()
