@@ -7,6 +7,8 @@
 // residual tiles are read with fully coalesced 16-byte loads, results leave as fully
 // coalesced 16-byte stores (a warp writes 4 fp32 rows x 128 B or 8 bf16 rows x 64 B per
 // instruction) instead of 32 scattered row segments.
+#include <cstdlib>
+
 #include "host_common.h"
 #include "tc_gemm.cuh"
 
@@ -180,36 +182,43 @@ static int launch_std(const CUtensorMap& ta, const CUtensorMap& talo, const CUte
   TileSched sched{(M + kBM - 1) / kBM, (N + BN - 1) / BN, 1, 1};
   epi.BN = BN;
   const cudaError_t e =
-      cluster == 2
-          ? launch_tc_gemm<BN, PASSES, gemm_stages<BN, PASSES, 2>(), 2>(
-                ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms())
-          : launch_tc_gemm<BN, PASSES, gemm_stages<BN, PASSES, 1>(), 1>(
-                ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms());
+      cluster == 4   ? launch_tc_gemm<BN, PASSES, gemm_stages<BN, PASSES, 4>(), 4>(
+                         ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms())
+      : cluster == 2 ? launch_tc_gemm<BN, PASSES, gemm_stages<BN, PASSES, 2>(), 2>(
+                         ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms())
+                     : launch_tc_gemm<BN, PASSES, gemm_stages<BN, PASSES, 1>(), 1>(
+                         ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms());
   ASTRA_CUDA_CHECK(e);
   return ASTRA_OK;
 }
 
-// Tile width: minimise (persistent waves x tile cost); narrow tiles pay ~15% more per column
-// (shared-memory operand bandwidth), 192 ~5%.
-static int pick_bn(int M, int N) {
+// Cluster shape and tile width.  Measured on B200 (scripts/gemm_bench.py): the 1-pass
+// mainloop moves ~29 B/clk of TMA operands per SM for every tile shape, and the 2x2 cluster
+// with A multicast does not raise that (and only 33 four-CTA clusters are co-resident, i.e.
+// 132 SMs), so the CTA pair is the default whenever there are two row blocks; cluster 4
+// stays selectable (ASTRA_GEMM_CLUSTER=4) for A/B runs.  Tile width minimises persistent
+// waves x tile cost (narrow tiles pay ~15% more per column, 192 ~5%).
+static void pick_tile(int M, int N, int* bn_out, int* cluster_out) {
   const int sms = num_sms();
   const int num_m = (M + kBM - 1) / kBM;
+  const int cl = num_m >= 2 ? 2 : 1;
   const int cands[3] = {256, 192, 128};
   const double eff[3] = {1.0, 1.05, 1.15};
-  int best = 128;
   double best_cost = 1e30;
+  *bn_out = 128;
+  *cluster_out = cl;
   for (int i = 0; i < 3; ++i) {
     const int bn = cands[i];
     if (bn > 128 && N < bn) continue;
-    const long tiles = (long)num_m * ((N + bn - 1) / bn);
-    const long waves = (tiles + sms - 1) / sms;
+    const long units = (long)((num_m + cl - 1) / cl) * ((N + bn - 1) / bn);
+    const long slots = sms / cl;
+    const long waves = (units + slots - 1) / slots;
     const double cost = (double)waves * bn * eff[i];
     if (cost < best_cost - 1e-9) {
       best_cost = cost;
-      best = bn;
+      *bn_out = bn;
     }
   }
-  return best;
 }
 
 }  // namespace astra
@@ -229,19 +238,23 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                 "astra_gemm: passes=3 needs lo operands");
   ASTRA_REQUIRE(out_lo == nullptr || out_hi != nullptr, ASTRA_ERR_SHAPE,
                 "astra_gemm: out_lo requires out_hi");
-  const int BN = pick_bn(M, N);
-  // pairs of CTAs share (multicast) the B tile whenever there are two row blocks to pair
-  const int cluster = (M > kBM) ? 2 : 1;
-  const int brows = BN / cluster;
+  int BN, cluster;
+  pick_tile(M, N, &BN, &cluster);
+  if (const char* f = getenv("ASTRA_GEMM_CLUSTER")) {   // A/B hook (benchmarks)
+    const int c = atoi(f);
+    if ((c == 1) || (c == 2 && M > kBM) || (c == 4 && M > kBM && (N + BN - 1) / BN >= 2)) cluster = c;
+  }
+  const int brows = cluster == 1 ? BN : BN / 2;
+  const int arows = cluster == 4 ? kBM / 2 : kBM;
   CUtensorMap ta, talo, tb, tblo;
   int st;
-  if ((st = make_tmap_2d(&ta, a_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, lda, kBM, kBK, true)))
+  if ((st = make_tmap_2d(&ta, a_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, lda, arows, kBK, true)))
     return st;
   if ((st = make_tmap_2d(&tb, b_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, K, ldb, brows, kBK,
                          true)))
     return st;
   if (passes == 3) {
-    if ((st = make_tmap_2d(&talo, a_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, lda, kBM, kBK,
+    if ((st = make_tmap_2d(&talo, a_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, K, lda, arows, kBK,
                            true)))
       return st;
     if ((st = make_tmap_2d(&tblo, b_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, N, K, ldb, brows, kBK,

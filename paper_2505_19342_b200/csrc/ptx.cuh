@@ -131,6 +131,21 @@ ASTRA_DEVICE void tma_load_2d_pair(void* smem_dst, const void* desc, uint32_t ba
       "l"(cache_hint)
       : "memory");
 }
+// CTA-pair load multicast to the CTAs in `mask`: the box lands at the same offset in each
+// destination and its bytes complete on the barrier at `bar_offset` in each destination's pair
+// leader (CUTLASS SM100_TMA_2SM_LOAD_MULTICAST convention: local barrier address with the
+// peer bit, bit 24, cleared).
+ASTRA_DEVICE void tma_load_2d_pair_mc(void* smem_dst, const void* desc, uint32_t bar_pair_addr,
+                                      int c0, int c1, uint16_t mask, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_pair_addr), "h"(mask), "r"(c0), "r"(c1),
+      "l"(cache_hint)
+      : "memory");
+}
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 // shared::cluster address of the same variable in CTA `rank` of the cluster
 ASTRA_DEVICE uint32_t mapa_shared(const void* p, uint32_t rank) {
   uint32_t r;
@@ -193,6 +208,15 @@ ASTRA_DEVICE void tmem_alloc(uint32_t* smem_slot) {
 template <uint32_t kCols>
 ASTRA_DEVICE void tmem_dealloc(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+// Per-warp register budget hand-off between warp roles (all warps of a warpgroup together).
+template <uint32_t kRegs>
+ASTRA_DEVICE void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+ASTRA_DEVICE void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
 }
 ASTRA_DEVICE void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 ASTRA_DEVICE void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

@@ -14,6 +14,8 @@
 // Two TMEM accumulators (2*BN columns) let the epilogue of tile i overlap the MMAs of tile i+1.
 #pragma once
 #include <cuda.h>
+#include <cstdio>
+#include <cstdlib>
 #include "ptx.cuh"
 
 namespace astra {
@@ -31,7 +33,7 @@ constexpr int kEpiStageBytes = 2048 + 64;   // per-epilogue-warp smem: 32x16 fp3
 template <int BN, int PASSES, int CLUSTER = 1>
 struct GemmSmem {
   static constexpr int kATile = kBM * kBK * 2;       // bytes
-  static constexpr int kBTile = (BN / CLUSTER) * kBK * 2;
+  static constexpr int kBTile = (CLUSTER == 1 ? BN : BN / 2) * kBK * 2;
   static constexpr int kOperands = (PASSES == 3) ? 2 : 1;
   static constexpr int kStageBytes = kOperands * (kATile + kBTile);
 };
@@ -52,15 +54,20 @@ struct TileCoord {
 // (m-fastest order re-read the 77 MB W2 operand from DRAM once per column tile).
 struct TileSched {
   int num_m, num_n, num_b;
-  int cluster;  // CTAs per cluster along M (1 or 2); a unit = `cluster` adjacent row blocks
-  __device__ int num_units_m() const { return (num_m + cluster - 1) / cluster; }
-  __device__ int total() const { return num_units_m() * num_n * num_b; }
+  int cluster;  // CTAs per cluster: 1, 2 (a pair along M) or 4 (two pairs along N)
+  __device__ int cm() const { return cluster >= 2 ? 2 : 1; }
+  __device__ int cn() const { return cluster == 4 ? 2 : 1; }
+  __device__ int num_units_m() const { return (num_m + cm() - 1) / cm(); }
+  __device__ int num_units_n() const { return (num_n + cn() - 1) / cn(); }
+  __device__ int total() const { return num_units_m() * num_units_n() * num_b; }
+  // rank bit 0 = row block within the pair, bit 1 = column tile within the cluster
   __device__ TileCoord get(int t, int rank) const {
     TileCoord c;
-    c.n_blk = t % num_n;
-    t /= num_n;
+    const int un = num_units_n();
+    c.n_blk = (t % un) * cn() + (rank >> 1);
+    t /= un;
     const int mu = num_units_m();
-    c.m_blk = (t % mu) * cluster + rank;
+    c.m_blk = (t % mu) * cm() + (rank & 1);
     c.batch = t / mu;
     return c;
   }
@@ -73,6 +80,12 @@ struct TileSched {
 //                              quarter (BN/4 columns)*/,
 //                              uint8_t* stage /*kEpiStageBytes of warp-private smem*/) const;
 // It reads its accumulator row via tmem_ld* (warp-collective) and writes results.
+//
+// CLUSTER == 4: two such pairs side by side along N.  The CTAs with the same row block in
+// both pairs need the same A tile: each loads half of it (64 rows) and multicasts it to both,
+// so per SM the TMA request traffic drops to (64 + BN/2) rows per k-step.  Bytes landing in a
+// pair complete on that pair's leader barrier; a stage is free once BOTH pairs' MMAs have
+// retired it (the leaders' commits are multicast to all four CTAs; empty count 2).
 //
 // CLUSTER == 2: a CTA pair (cta_group::2).  The two CTAs of a cluster own adjacent 128-row
 // blocks of one 256-row tile; each loads its A rows and HALF of the B tile into its own smem,
@@ -88,8 +101,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo,
                    int K, TileSched sched, int a_batch_rows, int b_batch_rows, Epi epi) {
   using S = GemmSmem<BN, PASSES, CLUSTER>;
-  static_assert(CLUSTER == 1 || CLUSTER == 2, "cluster of 1 or 2");
-  constexpr bool kPair = CLUSTER == 2;
+  static_assert(CLUSTER == 1 || CLUSTER == 2 || CLUSTER == 4, "cluster of 1, 2 or 4");
+  constexpr bool kPair = CLUSTER >= 2;
+  constexpr bool kQuad = CLUSTER == 4;
   constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                  : (2 * BN <= 256) ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -105,7 +119,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const int rank = kPair ? (int)cluster_ctarank() : 0;
-  const bool leader = rank == 0;
+  const bool leader = (rank & 1) == 0;   // issues the pair's UMMAs
+  const int pair_leader = rank & ~1;
   const int unit0 = blockIdx.x / CLUSTER, units = gridDim.x / CLUSTER;
   const int num_kb = (K + kBK - 1) / kBK;
   const int total = sched.total();
@@ -119,7 +134,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], kQuad ? 2 : 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
@@ -144,18 +159,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ producer (both CTAs)
-      const uint32_t full0 = kPair ? mapa_shared(full_bar, 0) : smem_u32(full_bar);
+      const uint32_t full0 = kPair ? mapa_shared(full_bar, pair_leader) : smem_u32(full_bar);
+      const uint16_t a_mask = (uint16_t)((1u << (rank & 1)) | (1u << ((rank & 1) + 2)));
+      const uint32_t full_pb = smem_u32(full_bar) & kPeerBitMask;   // multicast form
       int stage = 0;
       uint32_t phase = 0;
       for (int t = unit0; t < total; t += units) {
         TileCoord tc = sched.get(t, rank);
         const int arow = tc.batch * a_batch_rows + tc.m_blk * kBM;
-        const int brow = tc.batch * b_batch_rows + tc.n_blk * BN + rank * (BN / CLUSTER);
+        const int brow = tc.batch * b_batch_rows + tc.n_blk * BN + (kPair ? (rank & 1) * (BN / 2) : 0);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * S::kStageBytes;
           const int kc = kb * kBK;
-          if (kPair) {
+          if (kQuad) {
+            // this CTA's half of the A tile goes to both pairs; B half to itself
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
+            const uint32_t fb = full_pb + stage * 8, fl = full0 + stage * 8;
+            const int half = rank >> 1;
+            tma_load_2d_pair_mc(st + half * (S::kATile / 2), &tmA, fb, kc, arow + half * (kBM / 2),
+                                a_mask, kEvictNormal);
+            tma_load_2d_pair(st + S::kATile, &tmB, fl, kc, brow, kEvictLast);
+            if (PASSES == 3) {
+              tma_load_2d_pair_mc(st + S::kATile + S::kBTile + half * (S::kATile / 2), &tmAlo, fb,
+                                  kc, arow + half * (kBM / 2), a_mask, kEvictNormal);
+              tma_load_2d_pair(st + 2 * S::kATile + S::kBTile, &tmBlo, fl, kc, brow, kEvictLast);
+            }
+          } else if (kPair) {
             // both CTAs' bytes land on the leader's full barrier
             if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
             const uint32_t fb = full0 + stage * 8;
@@ -186,7 +216,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ------------------------------------------------------------ MMA issuer (leader)
-      constexpr uint32_t idesc = idesc_bf16_f32(kBM * CLUSTER, BN);
+      constexpr uint32_t idesc = idesc_bf16_f32(kBM * (kPair ? 2 : 1), BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -227,7 +257,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           // the smem slot is free once these MMAs retire (in both CTAs of a pair)
           if (kPair)
-            umma_commit_pair_mc(&empty_bar[stage], 0x3);
+            umma_commit_pair_mc(&empty_bar[stage], kQuad ? 0xF : 0x3);
           else
             umma_commit(&empty_bar[stage]);
           if (++stage == STAGES) {
@@ -237,7 +267,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         // accumulator ready for the epilogue (of both CTAs)
         if (kPair)
-          umma_commit_pair_mc(&tfull_bar[acc], 0x3);
+          umma_commit_pair_mc(&tfull_bar[acc], (uint16_t)(0x3u << pair_leader));
         else
           umma_commit(&tfull_bar[acc]);
         if (++acc == 2) {
@@ -253,7 +283,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int part = (warp - 2) / 4;
     const int col_begin = part * (BN / kEpiParts), col_end = col_begin + BN / kEpiParts;
     uint8_t* stage = epi_stage + (warp - 2) * kEpiStageBytes;
-    const uint32_t tempty0 = kPair ? mapa_shared(tempty_bar, 0) : 0u;
+    const uint32_t tempty0 = kPair ? mapa_shared(tempty_bar, pair_leader) : 0u;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = unit0; t < total; t += units) {
@@ -306,12 +336,10 @@ inline cudaError_t launch_tc_gemm(const CUtensorMap& ta, const CUtensorMap& talo
     configured = true;
   }
   sched.cluster = CLUSTER;
-  const long units_m = (sched.num_m + CLUSTER - 1) / CLUSTER;
-  const long total = units_m * sched.num_n * sched.num_b;
-  const long max_units = sms / CLUSTER;
-  const int grid = (int)((total < max_units ? total : max_units) * CLUSTER);
+  const int cm = CLUSTER >= 2 ? 2 : 1, cn = CLUSTER == 4 ? 2 : 1;
+  const long units_m = (sched.num_m + cm - 1) / cm;
+  const long total = units_m * ((sched.num_n + cn - 1) / cn) * sched.num_b;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kGemmThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -322,6 +350,22 @@ inline cudaError_t launch_tc_gemm(const CUtensorMap& ta, const CUtensorMap& talo
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // Persistent grid = the clusters that can be co-resident.  Clusters live inside one GPC, so
+  // with GPCs of odd / non-multiple SM counts fewer than sms / CLUSTER fit; launching more
+  // would run the surplus as a second, mostly empty wave.
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    cfg.gridDim = dim3(CLUSTER * (sms / CLUSTER), 1, 1);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) n = sms / CLUSTER;
+    max_clusters = n;
+    if (getenv("ASTRA_GEMM_VERBOSE"))
+      fprintf(stderr, "tc_gemm<BN=%d,P=%d,C=%d>: %d co-resident clusters (%d SMs)\n", BN, PASSES,
+              CLUSTER, n, sms);
+  }
+  const long max_units = max_clusters;
+  const int grid = (int)((total < max_units ? total : max_units) * CLUSTER);
+  cfg.gridDim = dim3(grid, 1, 1);
   return cudaLaunchKernelEx(&cfg, kern, ta, talo, tb, tblo, K, sched, a_batch_rows, b_batch_rows,
                             epi);
 }

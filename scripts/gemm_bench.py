@@ -1,5 +1,5 @@
 """Microbenchmark of astra_gemm vs torch.matmul (cuBLAS) on the block's GEMM shapes."""
-import sys, torch
+import os, sys, torch
 sys.path.insert(0, ".")
 from paper_2505_19342_b200 import kernels
 
@@ -19,10 +19,16 @@ for M, N, K in shapes:
     out = torch.empty(M, N, device="cuda"); outh = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     fl = 2 * M * N * K
     t1 = bench(lambda: kernels.gemm(a, b, out_hi=outh))
+    cl = {}
+    for c in ("2", "4"):
+        os.environ["ASTRA_GEMM_CLUSTER"] = c
+        cl[c] = bench(lambda: kernels.gemm(a, b, out_hi=outh))
+    del os.environ["ASTRA_GEMM_CLUSTER"]
+    print(f"   cluster2 {cl['2']*1e6:.1f}us {fl/cl['2']/1e12:.0f} TF/s | cluster4 {cl['4']*1e6:.1f}us {fl/cl['4']/1e12:.0f} TF/s", flush=True)
     t3 = bench(lambda: kernels.gemm(a, b, a_lo=al, b_lo=bl, out_f32=out))
     tc = bench(lambda: torch.matmul(a, b.T))
     bias = torch.randn(N, device="cuda")
-    tg = bench(lambda: kernels.gemm(a, b, bias=bias, gelu=True, out_hi=outh))
+    tg = bench(lambda: kernels.gemm(a, b, bias=bias, gelu=2, out_hi=outh))
     res = torch.randn(M, N, device="cuda")
     tr = bench(lambda: kernels.gemm(a, b, bias=bias, residual=res, out_f32=out))
     print(f"   +bias+gelu->bf16 {tg*1e6:.1f}us | +bias+residual->f32 {tr*1e6:.1f}us", flush=True)

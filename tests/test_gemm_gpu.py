@@ -52,3 +52,22 @@ def test_gemm_split3_fp32_class(cuda, M, N, K):
     assert rel < 2e-5, rel
     # hi/lo outputs reproduce the fp32 value to 2^-16
     assert ((hi.float() + lo.float()) - out).abs().max().item() <= 2 ** -15 * out.abs().max().item()
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "4"])
+@pytest.mark.parametrize("M,N,K", [(12608, 768, 768), (1000, 3072, 768), (300, 900, 256)])
+def test_gemm_cluster_shapes(cuda, monkeypatch, cluster, M, N, K):
+    """Every CTA-cluster shape of the persistent GEMM (single CTA, CTA pair, 2x2 with A
+    multicast) on ragged shapes, with the fused bias + residual epilogue."""
+    from paper_2505_19342_b200 import kernels
+    monkeypatch.setenv("ASTRA_GEMM_CLUSTER", cluster)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    b = torch.randn(N, K, device=cuda, generator=g).to(torch.bfloat16)
+    bias = torch.randn(N, device=cuda, generator=g)
+    res = torch.randn(M, N, device=cuda, generator=g)
+    out = torch.empty(M, N, device=cuda)
+    kernels.gemm(a, b, bias=bias, residual=res, out_f32=out)
+    ref = _ref(a.float(), b.float(), bias=bias, residual=res)
+    err = (out - ref).abs().max().item()
+    assert err <= 1e-4 * max(1.0, ref.abs().max().item()), err
