@@ -305,8 +305,12 @@ def main():
 
     # ---- per-kernel event timing (same kernels, eager, after the timed region)
     rt.vq_stats.zero_()
+    rt.collect_vq_stats = True
+    rt.forward()   # one eager pass with the exactness counters on
+    rt.collect_vq_stats = False
+    torch.cuda.synchronize()
+    vs = rt.vq_stats.cpu().numpy().astype(float)
     prof = _profile(rt, steps=3)
-    vs = rt.vq_stats.cpu().numpy().astype(float) / 3.0
     tokens_encoded = rt.n_content * L
     vq_stats = {"tokens_encoded_per_step": tokens_encoded,
                 "tokens_reranked_fp64": vs[0] + vs[1], "tokens_with_overflowed_chunk": vs[1],

@@ -22,13 +22,17 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
                                  float* __restrict__ x_norm) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
-  for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < M; row += gridDim.x * warps) {
+  // one row per warp, every row of the grid in flight at once (no grid-stride tail: the
+  // kernel is HBM-latency bound, and a second partial round doubles the exposed latency)
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  if (row < M) {
     const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * ldx);
     float4 v[VPL];
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) v[i] = __ldg(xr + lane + 32 * i);
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
-      v[i] = __ldg(xr + lane + 32 * i);
       s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
       if (xs_hi) {  // bf16 hi/lo split of the raw row: the VQ-encode GEMM operand
         __nv_bfloat16 h[4], l[4];
@@ -310,14 +314,15 @@ extern "C" int astra_layernorm_ex(const float* x, int M, int D, int ldx, const f
                    (!out_hi || ld_bf % 4 == 0) && (!xs_hi || ld_xs % 4 == 0) &&
                    ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   const int grid = grid_rows(M, 8);
+  const int grid1 = (M + 3) / 4;   // vector kernels: one row per warp, 4 warps per block
   if (vec && D == 768)
-    layernorm_kernel<6><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+    layernorm_kernel<6><<<grid1, 128, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
                                              ld_bf, xh, xl, ld_xs, x_norm);
   else if (vec && D == 1024)
-    layernorm_kernel<8><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+    layernorm_kernel<8><<<grid1, 128, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
                                              ld_bf, xh, xl, ld_xs, x_norm);
   else if (vec && D == 512)
-    layernorm_kernel<4><<<grid, 256, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+    layernorm_kernel<4><<<grid1, 128, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
                                              ld_bf, xh, xl, ld_xs, x_norm);
   else {
     ASTRA_REQUIRE(xs_hi == nullptr && x_norm == nullptr, ASTRA_ERR_SHAPE,

@@ -237,6 +237,7 @@ class AstraRuntime:
             ws = cb0.workspace_bytes(max(self.n_content, 1)) if cb0 else 1
         self.vq_ws = e(max(ws, 1), dt=torch.uint8)
         self.vq_stats = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.collect_vq_stats = False   # exactness counters (re-rank rate); off on the hot path
         if self.comm is not None:
             wmax = (B * max(self.sizes) * self.G * self.bits + 31) // 32
             self.wmax = max(wmax, 1)
@@ -351,11 +352,13 @@ class AstraRuntime:
                                  self.X.data_ptr(), D, self.xs_hi.data_ptr(),
                                  self.xs_lo.data_ptr(), D, self.xnorm.data_ptr(), R,
                                  self.content_rows.data_ptr(), self.n_content,
-                                 self.idx_local.data_ptr(), self.vq_stats.data_ptr(),
+                                 self.idx_local.data_ptr(),
+                                 self.vq_stats.data_ptr() if self.collect_vq_stats else None,
                                  self.vq_ws.data_ptr(), self.vq_ws.numel(), s)
                 else:
                     cb.encode(self.X, out=self.idx_local, rows=self.content_rows,
-                              workspace=self.vq_ws, stats=self.vq_stats)
+                              workspace=self.vq_ws,
+                              stats=self.vq_stats if self.collect_vq_stats else None)
         # 2. exchange + remote K/V view
         if self.has_remote:
             with self._op("exchange"):
