@@ -152,9 +152,12 @@ ASTRA_DEVICE uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// Remote arrive (CUTLASS ClusterBarrier form).  An explicit .release.cluster compiles to a
+// GPU-scope MEMBAR that waits for all of the warp's outstanding global stores — measured as the
+// top stall of the GEMM epilogue warps (their TMEM-empty signal only orders tcgen05.ld reads,
+// which tcgen05.fence::before_thread_sync already covers).
 ASTRA_DEVICE void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
 template <uint32_t kCols>
 ASTRA_DEVICE void tmem_alloc_pair(uint32_t* smem_slot) {
