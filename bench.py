@@ -242,11 +242,18 @@ def main():
     from paper_2505_19342_b200.cluster import partition_tokens
     from paper_2505_19342_b200.runtime import AstraRuntime, TorchDistExchange
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # ASTRA_BENCH_ONE_GPU=1: every rank on cuda:0 with the gloo exchange (functional check of
+    # the multi-rank path on a one-GPU box; NCCL refuses two ranks on one device)
+    one_gpu = os.environ.get("ASTRA_BENCH_ONE_GPU") == "1"
+    dev_index = 0 if one_gpu else local_rank
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     comm = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         comm = TorchDistExchange()
     peaks = _peaks()
     params, xs = _setup_params(dev)
@@ -259,7 +266,7 @@ def main():
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if one_gpu else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -276,7 +283,7 @@ def main():
             rt.graph = None
             graphed = False
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        clocks = Clocks(local_rank)
+        clocks = Clocks(dev_index)
         with clocks:   # sampler starts before the warm-up so every sample is taken under load
             for _ in range(args.warmup):
                 rt.run()
