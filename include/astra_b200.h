@@ -156,6 +156,14 @@ int astra_gather_rows(const float* src, int lds, const int32_t* idx, int rows, i
  * becomes remote row codes[t] (G = 1, codebook K/V table) or t (codes == NULL). */
 int astra_key_map(const int32_t* key_map, int n, const int32_t* codes, int32_t* key_src,
                   void* stream);
+/* G = 1 fused exchange tail (replaces astra_unpack_indices per sender + astra_key_map):
+ * remote keys read their code straight from the all-gathered packed payload — sender e's
+ * words start at words[e * wmax], code i of sender e at bit i * bits (LSB first); gofs[e] =
+ * first content slot of sender e (nsend + 1 entries).  Codes >= size set *err_flag and map to
+ * row 0 (caller raises IndexCorruptionError). */
+int astra_key_map_packed(const int32_t* key_map, int n, const uint32_t* words, int wmax, int bits,
+                         int size, const int32_t* gofs, int nsend, int32_t* key_src,
+                         int32_t* err_flag, void* stream);
 
 /* ------------------------------------------------------ greedy decoding
  * Generation on the device holding the last prompt token (cluster.py:297-308,

@@ -44,6 +44,7 @@ SIGNATURES: dict[str, list] = {
     "astra_replica_mean": [_vp, _c_int, _c_int, _c_int, _vp, _vp],
     "astra_gather_rows": [_vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp],
     "astra_key_map": [_vp, _c_int, _vp, _vp, _vp],
+    "astra_key_map_packed": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _vp, _vp],
     "astra_attention": [_vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp, _vp, _c_int,
                         _c_int, _c_int, _c_int, _c_int, _c_int, ctypes.c_float, _vp, _vp, _vp,
                         _c_int, _c_int, _c_int, _c_int, _vp],

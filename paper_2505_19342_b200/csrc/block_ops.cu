@@ -373,6 +373,47 @@ extern "C" int astra_gather_rows(const float* src, int lds, const int32_t* idx, 
   return ASTRA_OK;
 }
 
+// G = 1 exchange, fused: remote key -> codebook row straight from the all-gathered packed
+// words (sender e's payload at words[e * wmax]; its code i at bit i * bits), replacing the
+// per-sender unpack launches + key map.  Corrupt codes (>= K) raise *err and map to row 0.
+__global__ void key_map_packed_kernel(const int32_t* __restrict__ key_map, int n,
+                                      const uint32_t* __restrict__ words, int wmax, int bits, int K,
+                                      const int32_t* __restrict__ gofs, int nsend,
+                                      int32_t* __restrict__ key_src, int32_t* err) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int m = key_map[j];
+  if (m >= 0) {
+    key_src[j] = m;
+    return;
+  }
+  const int slot = -(m + 1);
+  int e = 0;
+  while (e + 1 < nsend && __ldg(gofs + e + 1) <= slot) ++e;
+  const long long b = (long long)e * wmax * 32 + (long long)(slot - __ldg(gofs + e)) * bits;
+  const uint32_t* wp = words + (b >> 5);
+  const int off = (int)(b & 31);
+  uint64_t pair = __ldg(wp);
+  if (off + bits > 32) pair |= (uint64_t)__ldg(wp + 1) << 32;
+  int code = (int)((pair >> off) & ((1ull << bits) - 1));
+  if (code >= K) {
+    atomicExch(err, 1);
+    code = 0;
+  }
+  key_src[j] = -(code + 1);
+}
+
+extern "C" int astra_key_map_packed(const int32_t* key_map, int n, const uint32_t* words, int wmax,
+                                    int bits, int size, const int32_t* gofs, int nsend,
+                                    int32_t* key_src, int32_t* err_flag, void* stream) {
+  ASTRA_REQUIRE(bits >= 1 && bits <= 31 && nsend >= 1, ASTRA_ERR_SHAPE, "key_map_packed: bad shape");
+  if (n == 0) return ASTRA_OK;
+  key_map_packed_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
+      key_map, n, words, wmax, bits, size, gofs, nsend, key_src, err_flag);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
 extern "C" int astra_key_map(const int32_t* key_map, int n, const int32_t* codes,
                              int32_t* key_src, void* stream) {
   if (n == 0) return ASTRA_OK;

@@ -244,6 +244,7 @@ class AstraRuntime:
             self.words_local = torch.zeros(self.wmax, dtype=torch.int32, device=dev)
             self.words_all = torch.zeros(self.N * self.wmax, dtype=torch.int32, device=dev)
             self.unpack_err = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.gofs_dev = torch.tensor(np.asarray(self.gofs, dtype=np.int32), device=dev)
         if self.has_remote and self.G > 1:
             n = self.n_content_all
             self.xhat = e(n, D)
@@ -316,17 +317,25 @@ class AstraRuntime:
         e.record()
         self.profile.setdefault(name, []).append((s, e))
 
-    def _exchange(self, layer: int):
-        """Make every device's layer-`layer` codes visible to this GPU (cluster.py:276-279)."""
+    def _exchange(self, layer: int) -> bool:
+        """Make every device's layer-`layer` codes visible to this GPU (cluster.py:276-279).
+        Returns True when the key map was already resolved from the packed payload (G = 1)."""
         if self.comm is None:
-            return
+            return False
         kernels.pack_indices(self.idx_local, self.bits, out=self.words_local)
         self.comm.all_gather(self.words_all, self.words_local)
+        if self.G == 1 and self.trace is None:
+            _native.call("astra_key_map_packed", self.key_map.data_ptr(), self.n_keys,
+                         self.words_all.data_ptr(), self.wmax, self.bits, self.K,
+                         self.gofs_dev.data_ptr(), self.N, self.key_src.data_ptr(),
+                         self.unpack_err.data_ptr(), _stream())
+            return True
         for e in range(self.N):
             cnt = self.B * self.sizes[e] * self.G
             kernels.unpack_indices(self.words_all[e * self.wmax:], cnt, self.bits, self.K,
                                    out=self.idx_all.view(-1)[int(self.gofs[e]) * self.G:],
                                    err=self.unpack_err)
+        return False
 
     def _layer(self, l: int):
         lay = self.layers[l]
@@ -362,10 +371,11 @@ class AstraRuntime:
         # 2. exchange + remote K/V view
         if self.has_remote:
             with self._op("exchange"):
-                self._exchange(l)
+                resolved = self._exchange(l)
             if self.G == 1:
-                _native.call("astra_key_map", self.key_map.data_ptr(), self.n_keys,
-                             self.idx_all.data_ptr(), self.key_src.data_ptr(), s)
+                if not resolved:
+                    _native.call("astra_key_map", self.key_map.data_ptr(), self.n_keys,
+                                 self.idx_all.data_ptr(), self.key_src.data_ptr(), s)
                 remote = lay["kvtab"]
             else:
                 cb.decode(self.idx_all, out=self.xhat, err=self.dec_err)
