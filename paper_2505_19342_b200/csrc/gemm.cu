@@ -197,13 +197,12 @@ static int launch_std(const CUtensorMap& ta, const CUtensorMap& talo, const CUte
 // with A multicast does not raise that (and only 33 four-CTA clusters are co-resident, i.e.
 // 132 SMs), so the CTA pair is the default whenever there are two row blocks; cluster 4
 // stays selectable (ASTRA_GEMM_CLUSTER=4) for A/B runs.  Tile width minimises persistent
-// waves x tile cost (narrow tiles pay ~15% more per column, 192 ~5%).
+// waves x per-SM operand rows per k-step (W1 12608x3072x768: BN 256 55.5 us vs 192 61.7 us).
 static void pick_tile(int M, int N, int* bn_out, int* cluster_out) {
   const int sms = num_sms();
   const int num_m = (M + kBM - 1) / kBM;
   const int cl = num_m >= 2 ? 2 : 1;
   const int cands[3] = {256, 192, 128};
-  const double eff[3] = {1.0, 1.05, 1.15};
   double best_cost = 1e30;
   *bn_out = 128;
   *cluster_out = cl;
@@ -213,7 +212,8 @@ static void pick_tile(int M, int N, int* bn_out, int* cluster_out) {
     const long units = (long)((num_m + cl - 1) / cl) * ((N + bn - 1) / bn);
     const long slots = sms / cl;
     const long waves = (units + slots - 1) / slots;
-    const double cost = (double)waves * bn * eff[i];
+    // a tile's k-step costs the operand rows this SM requests (ingress-bound mainloop)
+    const double cost = (double)waves * (cl == 2 ? 128 + bn / 2 : 128 + bn);
     if (cost < best_cost - 1e-9) {
       best_cost = cost;
       *bn_out = bn;
@@ -240,6 +240,10 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                 "astra_gemm: out_lo requires out_hi");
   int BN, cluster;
   pick_tile(M, N, &BN, &cluster);
+  if (const char* f = getenv("ASTRA_GEMM_BN")) {   // A/B hook (benchmarks)
+    const int b = atoi(f);
+    if ((b == 128 || b == 192 || b == 256) && (b == 128 || N >= b)) BN = b;
+  }
   if (const char* f = getenv("ASTRA_GEMM_CLUSTER")) {   // A/B hook (benchmarks)
     const int c = atoi(f);
     if ((c == 1) || (c == 2 && M > kBM) || (c == 4 && M > kBM && (N + BN - 1) / BN >= 2)) cluster = c;

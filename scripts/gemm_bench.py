@@ -20,11 +20,11 @@ for M, N, K in shapes:
     fl = 2 * M * N * K
     t1 = bench(lambda: kernels.gemm(a, b, out_hi=outh))
     cl = {}
-    for c in ("2", "4"):
-        os.environ["ASTRA_GEMM_CLUSTER"] = c
-        cl[c] = bench(lambda: kernels.gemm(a, b, out_hi=outh))
-    del os.environ["ASTRA_GEMM_CLUSTER"]
-    print(f"   cluster2 {cl['2']*1e6:.1f}us {fl/cl['2']/1e12:.0f} TF/s | cluster4 {cl['4']*1e6:.1f}us {fl/cl['4']/1e12:.0f} TF/s", flush=True)
+    for bn in ("128", "192", "256"):
+        os.environ["ASTRA_GEMM_BN"] = bn
+        cl[bn] = bench(lambda: kernels.gemm(a, b, out_hi=outh))
+    del os.environ["ASTRA_GEMM_BN"]
+    print("   " + " | ".join(f"BN{k} {v*1e6:.1f}us {fl/v/1e12:.0f} TF/s" for k, v in cl.items()), flush=True)
     t3 = bench(lambda: kernels.gemm(a, b, a_lo=al, b_lo=bl, out_f32=out))
     tc = bench(lambda: torch.matmul(a, b.T))
     bias = torch.randn(N, device="cuda")
