@@ -203,7 +203,10 @@ def _ncu_traffic(op):
 
 
 def _profile(rt, steps=3):
+    """Per-op device time of an eager forward with the VQ side stream folded back into the
+    main stream, so every op is timed in isolation (the graphed step overlaps them)."""
     import torch
+    rt.overlap_vq = False
     rt.profile = {}
     for _ in range(steps):
         rt.forward()
@@ -214,6 +217,7 @@ def _profile(rt, steps=3):
         out[name] = dict(total_ms=sum(ms) / steps, launches=len(ms) // steps,
                          avg_ms=sum(ms) / len(ms))
     rt.profile = None
+    rt.overlap_vq = True
     return out
 
 

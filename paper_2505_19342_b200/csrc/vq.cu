@@ -37,6 +37,8 @@ struct VqWorkspace {
   int* rec_cnt;       // [G, M, nchunk]
   int* rec_idx;       // [G, M, nchunk, cap]
   float* rec_score;   // [G, M, nchunk, cap]
+  int* rr_list;       // [G * M] items whose window holds > 1 candidate (fp64 re-rank)
+  int* rr_count;      // [1]
 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -56,6 +58,8 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
   size_t o_cnt = take((size_t)G * M * nchunk * 4);
   size_t o_idx = take((size_t)G * M * nchunk * kVqCap * 4);
   size_t o_sc = take((size_t)G * M * nchunk * kVqCap * 4);
+  size_t o_rl = take((size_t)G * M * 4);
+  size_t o_rc = take(4);
   if (w && base) {
     uint8_t* b = reinterpret_cast<uint8_t*>(base);
     w->x_hi = reinterpret_cast<__nv_bfloat16*>(b + o_hi);
@@ -65,6 +69,8 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
     w->rec_cnt = reinterpret_cast<int*>(b + o_cnt);
     w->rec_idx = reinterpret_cast<int*>(b + o_idx);
     w->rec_score = reinterpret_cast<float*>(b + o_sc);
+    w->rr_list = reinterpret_cast<int*>(b + o_rl);
+    w->rr_count = reinterpret_cast<int*>(b + o_rc);
   }
   return off;
 }
@@ -308,51 +314,136 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
     only = min(only, __shfl_xor_sync(0xffffffffu, only, o));
     overflow |= __shfl_xor_sync(0xffffffffu, overflow, o);
   }
-  int result = only;
   if (overflow || n > 1) {
+    // several window candidates: exact fp64 re-rank by vq_rerank_kernel
+    if (lane == 0) w.rr_list[atomicAdd(w.rr_count, 1)] = item;
+  } else if (lane == 0) {
+    idx_out[(size_t)row * G + g] = only;
+  }
+  if (lane == 0 && stats) atomicAdd(&stats[2], n);
+}
+
+// Exact fp64 re-rank of the listed items (one warp per item, grid-stride over the list): the
+// window's candidate codes are compacted into a per-warp list and each is scored with the
+// reference expression (||p||^2 - 2 p.c) + ||c||^2 (vq.py:130), ties to the lowest index.
+// For group widths <= 1024 each lane loads its slice of the token and of a candidate row in
+// one batch of independent loads (one memory round trip per candidate, not one per 32
+// elements); a chunk whose candidate list overflowed contributes all of its 64 codes.
+__global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const float* __restrict__ x,
+                                                        int M, int ldx,
+                                                        const int32_t* __restrict__ rows,
+                                                        VqWorkspace w, int nchunk,
+                                                        int32_t* __restrict__ idx_out,
+                                                        int32_t* __restrict__ stats, int Mrec,
+                                                        int rec_by_row) {
+  __shared__ int s_cand[8][32 * kVqCap];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int G = cb.groups, K = cb.size, gd = cb.group_dim;
+  const int total = *w.rr_count;
+  constexpr int kPartCodes = kVqBN / kEpiParts;
+  for (int li = blockIdx.x * 8 + wib; li < total; li += gridDim.x * 8) {
+    const int item = w.rr_list[li];
+    const int g = item / M, row = item % M;
+    const int rr = rec_by_row ? rows[row] : row;
+    const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
+    const float xn = w.x_norm[(size_t)g * Mrec + rr];
+    float best = INFINITY;
+    for (int c = lane; c < nchunk; c += 32) best = fminf(best, w.rec_best[rec0 + c]);
+    for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    const float thr = best + 2.0f * score_delta(xn, cb.c_norm_max[g]);
     const int src = rows ? rows[row] : row;
     const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
-    double pp = 0.0;
-    for (int e = lane; e < gd; e += 32) pp = fma((double)__ldg(xr + e), (double)__ldg(xr + e), pp);
-    pp = warp_sum_d(pp);
     const float* cents = cb.centroids + (size_t)g * K * gd;
     const double* cc = cb.c_sq64 + (size_t)g * K;
-    double bd = INFINITY;
-    int bi = -1;
-    // candidates in increasing code order; a chunk whose list overflowed contributes all of
-    // its codes (chunk c = tile c / kEpiParts, column part c % kEpiParts: 64 codes)
-    constexpr int kPartCodes = kVqBN / kEpiParts;
-    for (int c = 0; c < nchunk; ++c) {
-      if (w.rec_best[rec0 + c] > thr) continue;
-      const int m = w.rec_cnt[rec0 + c];
-      if (m > kVqCap) {
-        const int k_lo = (c / kEpiParts) * kVqBN + (c % kEpiParts) * kPartCodes;
-        const int k_hi = min(K, k_lo + kPartCodes);
-        for (int k = k_lo; k < k_hi; ++k) {
-          const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
-          if (d < bd || (d == bd && k < bi)) {
-            bd = d;
-            bi = k;
-          }
-        }
-        continue;
+    const bool vec = gd <= 1024;
+    float xs[32];   // this lane's slice of the token (fp32 inputs, fp64 arithmetic)
+    double pp = 0.0;
+    if (vec) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int e = lane + 32 * i;
+        xs[i] = e < gd ? __ldg(xr + e) : 0.0f;
       }
-      for (int i = 0; i < m; ++i) {
-        if (w.rec_score[(rec0 + c) * kVqCap + i] > thr) continue;
-        const int k = w.rec_idx[(rec0 + c) * kVqCap + i];
-        const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
-        if (d < bd || (d == bd && k < bi)) {
-          bd = d;
-          bi = k;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) pp = fma((double)xs[i], (double)xs[i], pp);
+    } else {
+      for (int e = lane; e < gd; e += 32) pp = fma((double)__ldg(xr + e), (double)__ldg(xr + e), pp);
+    }
+    pp = warp_sum_d(pp);
+    double bd = INFINITY;
+    int bi = -1, overflowed = 0;
+    auto score = [&](int k) {
+      const float* c = cents + (size_t)k * gd;
+      double pc = 0.0;
+      if (vec) {
+        float cv[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int e = lane + 32 * i;
+          cv[i] = e < gd ? __ldg(c + e) : 0.0f;
         }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pc = fma((double)xs[i], (double)cv[i], pc);
+      } else {
+        for (int e = lane; e < gd; e += 32) pc = fma((double)__ldg(xr + e), (double)__ldg(c + e), pc);
+      }
+      pc = warp_sum_d(pc);
+      const double d = (pp - 2.0 * pc) + cc[k];
+      if (d < bd || (d == bd && k < bi)) {
+        bd = d;
+        bi = k;
+      }
+    };
+    // candidates of the window, chunk by chunk (lane c reads chunk c), compacted in order
+    for (int c0 = 0; c0 < nchunk; c0 += 32) {
+      const int c = c0 + lane;
+      uint32_t live = 0;
+      int ix[kVqCap];
+      int full_part = 0;
+      if (c < nchunk && w.rec_best[rec0 + c] <= thr) {
+        const int m = w.rec_cnt[rec0 + c];
+        if (m > kVqCap) {
+          full_part = 1;
+        } else {
+#pragma unroll
+          for (int i = 0; i < kVqCap; ++i)
+            if (i < m && w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
+              live |= 1u << i;
+              ix[i] = w.rec_idx[(rec0 + c) * kVqCap + i];
+            }
+        }
+      }
+      const int cnt = __popc(live);
+      int pre = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += t;
+      }
+      const int tot = __shfl_sync(0xffffffffu, pre, 31);
+      pre -= cnt;
+      int k_ = 0;
+#pragma unroll
+      for (int i = 0; i < kVqCap; ++i)
+        if ((live >> i) & 1u) s_cand[wib][pre + k_++] = ix[i];
+      __syncwarp();
+      for (int q = 0; q < tot; ++q) score(s_cand[wib][q]);
+      __syncwarp();
+      // overflowed chunks: every code of the 64-code part (rare; exact in any order since
+      // ties resolve to the lowest index)
+      uint32_t fb = __ballot_sync(0xffffffffu, full_part);
+      overflowed |= fb != 0;
+      while (fb) {
+        const int cc_ = c0 + __ffs(fb) - 1;
+        fb &= fb - 1;
+        const int k_lo = (cc_ / kEpiParts) * kVqBN + (cc_ % kEpiParts) * kPartCodes;
+        const int k_hi = min(K, k_lo + kPartCodes);
+        for (int k = k_lo; k < k_hi; ++k) score(k);
       }
     }
-    result = bi;
-    if (stats && lane == 0) atomicAdd(&stats[overflow ? 1 : 0], 1);
-  }
-  if (lane == 0) {
-    idx_out[(size_t)row * G + g] = result;
-    if (stats) atomicAdd(&stats[2], n);
+    if (lane == 0) {
+      idx_out[(size_t)row * G + g] = bi;
+      if (stats) atomicAdd(&stats[overflowed ? 1 : 0], 1);
+    }
   }
 }
 
@@ -476,8 +567,12 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
                                                     num_sms());
   ASTRA_CUDA_CHECK(e);
   const int items = G * M;
+  ASTRA_CUDA_CHECK(cudaMemsetAsync(w.rr_count, 0, sizeof(int), s));
   vq_finalize_kernel<<<(items + 7) / 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                       stats, Mg, rec_by_row);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  vq_rerank_kernel<<<num_sms() * 2, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
+                                                 Mg, rec_by_row);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }

@@ -114,6 +114,9 @@ class AstraRuntime:
         self._build_layout()
         self._upload(params)
         self._alloc()
+        self.side_stream = torch.cuda.Stream(device=self.device)
+        self.overlap_vq = True   # False: strictly sequential launches (isolated kernel timing)
+        self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
         self.graph = None
         self.graphs = []
         self.x_slots = [self.x_in]
@@ -353,7 +356,40 @@ class AstraRuntime:
                          self.ln_hi.data_ptr(), _p(self.ln_lo), D,
                          _p(self.xs_hi) if split else None, _p(self.xs_lo) if split else None, D,
                          _p(self.xnorm) if split else None, s)
-        # 2. VQ encode of this GPU's content tokens (cluster.py:272-275)
+        # 2. VQ encode of this GPU's content tokens (cluster.py:272-275) and the exchange run on a
+        #    side stream, overlapping the Q|K|V GEMM (the latency-bound finalize / re-rank
+        #    kernels co-reside with the GEMM's CTAs).  They read X and the split LN1 wrote; the
+        #    main stream joins before attention (N > 1: the remote keys) or before W2 (N = 1:
+        #    W2 overwrites X).
+        main = torch.cuda.current_stream()
+        side_work = (encode or self.has_remote) and self.overlap_vq
+        if side_work:
+            self._ev_fork.record(main)
+            self.side_stream.wait_event(self._ev_fork)
+        side_ctx = torch.cuda.stream(self.side_stream) if side_work else contextlib.nullcontext()
+        with side_ctx:
+            remote = self._encode_exchange(l, lay, cb, encode, split)
+            if side_work:
+                self._ev_join.record(self.side_stream)
+        if side_work and self.trace is not None:
+            main.wait_event(self._ev_join)   # test hook reads the codes now
+            self.trace.append(self.idx_all.clone())
+        elif self.trace is not None:
+            self.trace.append(self.idx_all.clone())
+        # 4. fused Q|K|V projection
+        whi, wlo = lay["wqkv"]
+        with self._op("gemm_qkv"):
+            kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo,
+                         out_f32=None if self.fast else self.qkv,
+                         out_hi=self.qkv if self.fast else None)
+        joined = not side_work or self.trace is not None
+        self._layer_rest(l, lay, remote, join_before_attn=not joined and self.has_remote,
+                         join_before_w2=not joined and not self.has_remote)
+
+    def _encode_exchange(self, l, lay, cb, encode, split):
+        """VQ encode + exchange + remote K/V view (on the current stream); returns the remote
+        K/V buffer for the attention kernel."""
+        D, R, s = self.D, self.R, _stream()
         if encode:
             with self._op("vq_encode"):
                 if split:
@@ -383,14 +419,12 @@ class AstraRuntime:
                 remote = self.kvhat
         else:
             remote = self.qkv
-        if self.trace is not None:
-            self.trace.append(self.idx_all.clone())
-        # 4. fused Q|K|V projection
-        whi, wlo = lay["wqkv"]
-        with self._op("gemm_qkv"):
-            kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo,
-                         out_f32=None if self.fast else self.qkv,
-                         out_hi=self.qkv if self.fast else None)
+        return remote
+
+    def _layer_rest(self, l, lay, remote, join_before_attn: bool, join_before_w2: bool):
+        D, R, s = self.D, self.R, _stream()
+        if join_before_attn:
+            torch.cuda.current_stream().wait_event(self._ev_join)   # remote keys resolved
         if self.mode == "generate" and self.decodes:
             # DecodeState capture (cluster.py:285-288): device N-1's K|V view of the prompt
             e = self.ebytes
@@ -424,6 +458,8 @@ class AstraRuntime:
             kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo, bias=lay["b1"], gelu=self.gelu_mode,
                          out_hi=self.f_hi, out_lo=self.f_lo)
         whi, wlo = lay["w2"]
+        if join_before_w2:
+            torch.cuda.current_stream().wait_event(self._ev_join)   # VQ reads of X are done
         with self._op("gemm_w2"):
             kernels.gemm(self.f_hi, whi, a_lo=self.f_lo, b_lo=wlo, bias=lay["b2"],
                          residual=self.Hres, out_f32=self.X)
