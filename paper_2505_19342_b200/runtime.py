@@ -79,6 +79,22 @@ class TorchDistExchange:
         t.copy_(h)
 
 
+class LoopbackExchange:
+    """Stand-in for one rank of an N-rank run on a single GPU (timing tool): every rank's slot
+    of an all-gather receives this rank's own payload, a broadcast is a no-op.  The rank does
+    exactly the work it would do under torchrun minus the NCCL transfer; its numerical
+    results are not those of the real N-rank run."""
+
+    def __init__(self, rank: int, world: int):
+        self.rank, self.world = rank, world
+
+    def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        out.view(self.world, -1).copy_(inp.reshape(1, -1).expand(self.world, -1))
+
+    def broadcast(self, t: torch.Tensor, src: int) -> None:
+        return None
+
+
 class AstraRuntime:
     def __init__(self, params, plan, batch: int, mode: str = "classify",
                  cls_mode: str = "distributed", precision: str = "parity", comm=None,
@@ -541,7 +557,7 @@ class AstraRuntime:
             self._slot = slot
             self.forward()
             self._slot = 0
-        return self.logits
+        return getattr(self, "logits", None)
 
     def classify_stream(self, batches, out=None):
         """Serve a sequence of host batches ([B, T, D] fp32, pinned for async copies).

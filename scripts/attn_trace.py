@@ -34,7 +34,7 @@ ms = [s.elapsed_time(e) for s, e in rt.profile["attention"]]
 print("attention ms", ms)
 t = buf.view(32, 16).cpu().numpy().astype(np.int64)
 t0 = t[t > 0].min()
-names = ["0qk", "0S", "0PV", "0sm_st", "0sm_end", "0Sdone", "0pgo", "0top", "1qk", "1S", "1PV", "1sm_st", "1sm_end", "1Sdone", "1pgo", "1top"]
+names = ["0p2end", "0S", "0PV", "0sm_st", "0sm_end", "0Sdone", "0p1end", "0top", "1p2end", "1S", "1PV", "1sm_st", "1sm_end", "1Sdone", "1p1end", "1top"]
 print("unit " + " ".join(f"{x:>8s}" for x in names))
 for u in range(32):
     if t[u].max() == 0:

@@ -13,13 +13,15 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2505_19342_b200 import cluster, data, model, vq  # noqa: E402
-from paper_2505_19342_b200.runtime import AstraRuntime  # noqa: E402
+from paper_2505_19342_b200.runtime import AstraRuntime, LoopbackExchange  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1)
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--parity", action="store_true")
 ap.add_argument("--iters", type=int, default=1)
+ap.add_argument("--rank-of", type=int, default=0,
+                help="profile ONE rank (the last) of an N-way split, loopback exchange")
 args = ap.parse_args()
 
 cfg = model.ModelConfig(layers=12, hidden=768, heads=12, vocab_or_classes=1000, max_tokens=197,
@@ -28,8 +30,11 @@ params = model.init_params(cfg, seed=0)
 xs = data.make_classify_batch(768, 196, args.batch, seed=1)
 from paper_2505_19342_b200 import codebooks  # noqa: E402
 codebooks.fit_codebooks(params, data.make_classify_batch(768, 196, 8, seed=0), iterations=8)
-plan = cluster.partition_tokens(196, args.n)
-rt = AstraRuntime(params, plan, batch=args.batch, precision="parity" if args.parity else "fast")
+n = args.rank_of or args.n
+plan = cluster.partition_tokens(196, n)
+comm = LoopbackExchange(n - 1, n) if args.rank_of > 1 else None
+rt = AstraRuntime(params, plan, batch=args.batch, precision="parity" if args.parity else "fast",
+                  comm=comm)
 rt.stage_input(xs)
 torch.cuda.synchronize()
 rt.forward()                       # warm-up (module load, first-touch)
