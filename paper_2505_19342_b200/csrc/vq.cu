@@ -25,8 +25,11 @@
 
 namespace astra {
 
-constexpr int kVqBN = 256;
+constexpr int kVqBN = 256;      // distance-GEMM tile width (codes); 128 for small token counts
+constexpr int kVqBNMin = 128;
 constexpr int kVqCap = 4;          // candidates recorded per (row, chunk)
+constexpr int kRRCands = 8;        // candidates handed to the re-rank kernel directly
+constexpr int kRREntry = 2 + kRRCands;
 constexpr float kTau = 1.0f / 16384.0f;
 
 struct VqWorkspace {
@@ -37,14 +40,15 @@ struct VqWorkspace {
   int* rec_cnt;       // [G, M, nchunk]
   int* rec_idx;       // [G, M, nchunk, cap]
   float* rec_score;   // [G, M, nchunk, cap]
-  int* rr_list;       // [G * M] items whose window holds > 1 candidate (fp64 re-rank)
+  int* rr_list;       // [G * M][kRREntry] items whose window holds > 1 candidate (fp64 re-rank):
+                      // {item, n (-1: scan the records), candidate codes ...}
   int* rr_count;      // [1]
 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
-  const int nchunk = kEpiParts * ((K + kVqBN - 1) / kVqBN);
+  const int nchunk = kEpiParts * ((K + kVqBNMin - 1) / kVqBNMin);   // sized for the narrow tile
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -58,7 +62,7 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
   size_t o_cnt = take((size_t)G * M * nchunk * 4);
   size_t o_idx = take((size_t)G * M * nchunk * kVqCap * 4);
   size_t o_sc = take((size_t)G * M * nchunk * kVqCap * 4);
-  size_t o_rl = take((size_t)G * M * 4);
+  size_t o_rl = take((size_t)G * M * kRREntry * 4);
   size_t o_rc = take(4);
   if (w && base) {
     uint8_t* b = reinterpret_cast<uint8_t*>(base);
@@ -153,8 +157,9 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
 }
 
 // ---------------------------------------------------------- epilogue
+template <int BN>
 struct VqEpilogue {
-  int M, K, nchunk;         // nchunk = records per (g, row): kEpiParts per 256-code tile
+  int M, K, nchunk;         // nchunk = records per (g, row): kEpiParts per BN-code tile
   const float* c_sq;        // [G, K]
   const float* c_norm_max;  // [G]
   VqWorkspace w;
@@ -164,7 +169,7 @@ struct VqEpilogue {
     const int row = tc.m_blk * kBM + row_in_tile;
     const bool ok = row < M;
     const int g = tc.batch;
-    const int col_base = tc.n_blk * kVqBN;
+    const int col_base = tc.n_blk * BN;
     const float* csq = c_sq + (size_t)g * K;
     float best = INFINITY;
     // ||c||^2 of the 32 columns of a chunk: one coalesced load per warp, broadcast from smem
@@ -269,9 +274,11 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
   int n = 0, only = 0x7FFFFFFF;
   int overflow = 0;
   float thr = 0.f;
+  uint32_t live = 0;
+  int ix[kVqCap];
   if (nchunk <= 32) {
     float rb = INFINITY, sc[kVqCap];
-    int rc = 0, ix[kVqCap];
+    int rc = 0;
     if (lane < nchunk) {
       rb = w.rec_best[rec0 + lane];
       rc = w.rec_cnt[rec0 + lane];
@@ -291,9 +298,11 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
         if (i < rc && sc[i] <= thr) {
           ++n;
           only = min(only, ix[i]);
+          live |= 1u << i;
         }
     }
   } else {
+    overflow = 1;   // wide codebooks: the re-rank kernel scans the records
     for (int c = lane; c < nchunk; c += 32) best = fminf(best, w.rec_best[rec0 + c]);
     for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
     thr = best + 2.0f * score_delta(xn, cmax);
@@ -315,8 +324,29 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
     overflow |= __shfl_xor_sync(0xffffffffu, overflow, o);
   }
   if (overflow || n > 1) {
-    // several window candidates: exact fp64 re-rank by vq_rerank_kernel
-    if (lane == 0) w.rr_list[atomicAdd(w.rr_count, 1)] = item;
+    // several window candidates: exact fp64 re-rank by vq_rerank_kernel, handed the compacted
+    // candidate list (codes in increasing order) when it fits
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(w.rr_count, 1);
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    int* ent = w.rr_list + (size_t)slot * kRREntry;
+    const bool direct = !overflow && n <= kRRCands;
+    if (direct) {
+      const int cnt = __popc(live);
+      int pre = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += t;
+      }
+      pre -= cnt;
+#pragma unroll
+      for (int i = 0; i < kVqCap; ++i)
+        if ((live >> i) & 1u) ent[2 + pre++] = ix[i];
+    }
+    if (lane == 0) {
+      ent[0] = item;
+      ent[1] = direct ? n : -1;
+    }
   } else if (lane == 0) {
     idx_out[(size_t)row * G + g] = only;
   }
@@ -335,15 +365,70 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
                                                         VqWorkspace w, int nchunk,
                                                         int32_t* __restrict__ idx_out,
                                                         int32_t* __restrict__ stats, int Mrec,
-                                                        int rec_by_row) {
+                                                        int rec_by_row, int part_codes) {
   __shared__ int s_cand[8][32 * kVqCap];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int G = cb.groups, K = cb.size, gd = cb.group_dim;
   const int total = *w.rr_count;
-  constexpr int kPartCodes = kVqBN / kEpiParts;
   for (int li = blockIdx.x * 8 + wib; li < total; li += gridDim.x * 8) {
-    const int item = w.rr_list[li];
+    const int* ent = w.rr_list + (size_t)li * kRREntry;
+    const int ev = __ldg(ent + min(lane, kRREntry - 1));   // whole entry in one round trip
+    const int item = __shfl_sync(0xffffffffu, ev, 0);
+    const int nd = __shfl_sync(0xffffffffu, ev, 1);
     const int g = item / M, row = item % M;
+    if (nd > 0 && cb.group_dim <= 1024) {
+      // direct: token slice and two candidate rows per round trip, fp64 dot products
+      const int src = rows ? rows[row] : row;
+      const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
+      const float* cents = cb.centroids + (size_t)g * K * gd;
+      float xs[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int e = lane + 32 * i;
+        xs[i] = e < gd ? __ldg(xr + e) : 0.0f;
+      }
+      double pp = 0.0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) pp = fma((double)xs[i], (double)xs[i], pp);
+      pp = warp_sum_d(pp);
+      double bd = INFINITY;
+      int bi = -1;
+      for (int q = 0; q < nd; q += 2) {
+        const int k0 = __shfl_sync(0xffffffffu, ev, 2 + q);
+        const int k1 = q + 1 < nd ? __shfl_sync(0xffffffffu, ev, 3 + q) : k0;
+        const float* c0p = cents + (size_t)k0 * gd;
+        const float* c1p = cents + (size_t)k1 * gd;
+        float c0[32], c1[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int e = lane + 32 * i;
+          c0[i] = e < gd ? __ldg(c0p + e) : 0.0f;
+          c1[i] = e < gd ? __ldg(c1p + e) : 0.0f;
+        }
+        const double cc0 = cb.c_sq64[(size_t)g * K + k0], cc1 = cb.c_sq64[(size_t)g * K + k1];
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          d0 = fma((double)xs[i], (double)c0[i], d0);
+          d1 = fma((double)xs[i], (double)c1[i], d1);
+        }
+        d0 = (pp - 2.0 * warp_sum_d(d0)) + cc0;
+        d1 = (pp - 2.0 * warp_sum_d(d1)) + cc1;
+        if (d0 < bd || (d0 == bd && k0 < bi)) {
+          bd = d0;
+          bi = k0;
+        }
+        if (d1 < bd || (d1 == bd && k1 < bi)) {
+          bd = d1;
+          bi = k1;
+        }
+      }
+      if (lane == 0) {
+        idx_out[(size_t)row * G + g] = bi;
+        if (stats) atomicAdd(&stats[0], 1);
+      }
+      continue;
+    }
     const int rr = rec_by_row ? rows[row] : row;
     const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
     const float xn = w.x_norm[(size_t)g * Mrec + rr];
@@ -435,8 +520,8 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       while (fb) {
         const int cc_ = c0 + __ffs(fb) - 1;
         fb &= fb - 1;
-        const int k_lo = (cc_ / kEpiParts) * kVqBN + (cc_ % kEpiParts) * kPartCodes;
-        const int k_hi = min(K, k_lo + kPartCodes);
+        const int k_lo = cc_ * part_codes;   // chunk c = codes [c * part, (c + 1) * part)
+        const int k_hi = min(K, k_lo + part_codes);
         for (int k = k_lo; k < k_hi; ++k) score(k);
       }
     }
@@ -536,14 +621,39 @@ extern "C" int64_t astra_vq_encode_workspace(int M, int groups, int size, int pa
 // Distance GEMM + windowed-argmin epilogue over `Mg` operand rows (per group), then the
 // finalize over the M tokens.  rec_by_row: records are indexed by source row (pre-split
 // operands cover the whole stack) instead of by token.
+template <int BN>
+static cudaError_t vq_launch_gemm(const AstraCodebook& cb, const CUtensorMap& ta,
+                                  const CUtensorMap& talo, int Mg, VqWorkspace w, int nchunk,
+                                  int cluster, cudaStream_t s) {
+  const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
+  CUtensorMap tb, tblo;
+  if (make_tmap_2d(&tb, cb.c_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp, gdp,
+                   BN / cluster, kBK, true) ||
+      make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp, gdp,
+                   BN / cluster, kBK, true))
+    return cudaErrorInvalidValue;
+  VqEpilogue<BN> epi{Mg, K, nchunk, cb.c_sq, cb.c_norm_max, w};
+  TileSched sched{(Mg + kBM - 1) / kBM, (K + BN - 1) / BN, G, 1};
+  return cluster == 2 ? launch_tc_gemm<BN, 3, 3, 2>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi, s,
+                                                    num_sms())
+                      : launch_tc_gemm<BN, 3, 2, 1>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi, s,
+                                                    num_sms());
+}
+
+// Distance GEMM + windowed-argmin epilogue over `Mg` operand rows (per group), then the
+// finalize over the M tokens.  rec_by_row: records are indexed by source row (pre-split
+// operands cover the whole stack) instead of by token.  Few token rows (one rank of a wide
+// split) take 128-code tiles so the persistent grid still covers the SMs.
 static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const void* a_lo, int lda,
                             int Mg, VqWorkspace w, const float* x, int M, int ldx,
                             const int32_t* rows, int rec_by_row, int32_t* idx_out, int32_t* stats,
                             cudaStream_t s) {
   const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
-  const int ntile = (K + kVqBN - 1) / kVqBN;
-  const int nchunk = kEpiParts * ntile;   // one record per epilogue column part
-  CUtensorMap ta, talo, tb, tblo;
+  const int cluster = (Mg > kBM) ? 2 : 1;  // CTA pairs split the codebook tile (cta_group::2)
+  const long units256 = (long)G * ((Mg + kBM * cluster - 1) / (kBM * cluster)) * ((K + kVqBN - 1) / kVqBN);
+  const int bn = (units256 * 2 * cluster <= num_sms()) ? kVqBNMin : kVqBN;
+  const int nchunk = kEpiParts * ((K + bn - 1) / bn);   // one record per epilogue column part
+  CUtensorMap ta, talo;
   int st;
   if ((st = make_tmap_2d(&ta, a_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * Mg, gdp,
                          lda, kBM, kBK, true)))
@@ -551,20 +661,8 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
   if ((st = make_tmap_2d(&talo, a_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * Mg, gdp,
                          lda, kBM, kBK, true)))
     return st;
-  const int cluster = (Mg > kBM) ? 2 : 1;  // CTA pairs split the codebook tile (cta_group::2)
-  if ((st = make_tmap_2d(&tb, cb.c_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
-                         gdp, kVqBN / cluster, kBK, true)))
-    return st;
-  if ((st = make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp,
-                         gdp, kVqBN / cluster, kBK, true)))
-    return st;
-  VqEpilogue epi{Mg, K, nchunk, cb.c_sq, cb.c_norm_max, w};
-  TileSched sched{(Mg + kBM - 1) / kBM, ntile, G, 1};
-  const cudaError_t e =
-      cluster == 2 ? launch_tc_gemm<kVqBN, 3, 3, 2>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi, s,
-                                                    num_sms())
-                   : launch_tc_gemm<kVqBN, 3, 2, 1>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi, s,
-                                                    num_sms());
+  const cudaError_t e = bn == kVqBN ? vq_launch_gemm<kVqBN>(cb, ta, talo, Mg, w, nchunk, cluster, s)
+                                    : vq_launch_gemm<kVqBNMin>(cb, ta, talo, Mg, w, nchunk, cluster, s);
   ASTRA_CUDA_CHECK(e);
   const int items = G * M;
   ASTRA_CUDA_CHECK(cudaMemsetAsync(w.rr_count, 0, sizeof(int), s));
@@ -572,7 +670,7 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
                                                       stats, Mg, rec_by_row);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   vq_rerank_kernel<<<num_sms() * 2, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
-                                                 Mg, rec_by_row);
+                                                 Mg, rec_by_row, bn / kEpiParts);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
