@@ -130,7 +130,8 @@ class AstraRuntime:
         self._build_layout()
         self._upload(params)
         self._alloc()
-        self.side_stream = torch.cuda.Stream(device=self.device)
+        # the VQ / exchange branch is on the critical path at N > 1: high stream priority
+        self.side_stream = torch.cuda.Stream(device=self.device, priority=-1)
         self.overlap_vq = True   # False: strictly sequential launches (isolated kernel timing)
         self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
         self.graph = None
