@@ -186,7 +186,8 @@ def _kernel_work(rt):
         "gemm_w1": dict(flops=2 * R * 4 * Dm * Dm, bytes=(R * Dm + 4 * Dm * Dm + 4 * R * Dm) * 2),
         "gemm_w2": dict(flops=2 * R * 4 * Dm * Dm, bytes=(4 * R * Dm + 4 * Dm * Dm) * 2 + R * Dm * 8),
         "attention": dict(flops=att_flops, bytes=att_bytes),
-        "ln1": dict(flops=0, bytes=R * Dm * (4 + 2)),
+        # LN1 also writes the bf16 hi/lo split of the raw rows and their norms (VQ operand)
+        "ln1": dict(flops=0, bytes=R * Dm * (4 + 2 + (4 if rt.presplit else 0)) + (R * 4 if rt.presplit else 0)),
         "ln2": dict(flops=0, bytes=R * Dm * (4 + 2)),
     }
 
