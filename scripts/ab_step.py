@@ -39,4 +39,4 @@ for _ in range(5):
 torch.cuda.synchronize()
 ops = {k: np.median([a.elapsed_time(b) for a, b in v]) * 1000 for k, v in rt.profile.items()}
 print(f"{Path(os.environ.get('ASTRA_B200_LIB', 'default')).name}: step {step:.4f} ms | " +
-      " ".join(f"{k} {v:.1f}" for k, v in ops.items() if k in ("attention", "vq_encode", "gemm_w1")))
+      " ".join(f"{k} {v:.1f}" for k, v in ops.items() if k.startswith("gemm")))
