@@ -89,6 +89,8 @@ def load():
         fn.restype = _RESTYPES.get(name, ctypes.c_int)
     if lib.astra_abi_version() != ABI_VERSION:
         raise NativeLibraryMissing("native library ABI mismatch; rebuild it")
+    if os.environ.get("ASTRA_ATTN_VARIANT"):   # A/B hook: attention kernel variant
+        lib.astra_attention_variant(int(os.environ["ASTRA_ATTN_VARIANT"]))
     _lib = lib
     return lib
 

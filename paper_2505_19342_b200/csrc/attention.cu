@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
 // K/V table rows) into the tile load.
 constexpr int kTQ = 128, kTKC = 256, kTcThreads = 256;
 static bool g_force_simt_attention = false;  // test hook (astra_attention_force_simt)
-static int g_attention_variant = 0;  // 0 persistent tcgen05, 1 one CTA per tile (astra_attention_variant)
+static int g_attention_variant = 0;  // 0 persistent two pipelines, 1 one CTA per tile, 2 persistent single pipeline + correction warps
 // Q 16 KB + K 32 KB + V 32 KB + 256 key positions + row max / sum exchange (4 x 128 floats)
 // + barrier and TMEM slot, plus 1 KB to align the base for the SW128 layouts.
 constexpr int kTcSmemUsed = 16384 + 32768 + 32768 + 512 + 2048 + 64;
@@ -526,7 +526,7 @@ struct PItem {
   int q0, nq, qpos0, ncontent, k0, nk, h, qt;
 };
 struct PUnit {
-  int q0, nq, qpos0, ncontent, k0, nk, h, qt, kc;
+  int q0, nq, qpos0, ncontent, k0, nk, h, qt, kc, cs;   // cs: keys per chunk
   bool ok;
 };
 __device__ __forceinline__ PItem p_decode(const AttnArgs& a, int qtiles, int t) {
@@ -543,12 +543,12 @@ __device__ __forceinline__ PItem p_decode(const AttnArgs& a, int qtiles, int t) 
   return r;
 }
 struct PIter {
-  int i, n_items, qtiles;
+  int i, n_items, qtiles, step = 2, cs = kTKC;
   const PItem* table;
   PUnit cur;
   __device__ __forceinline__ void next_item(const AttnArgs& a) {
     cur.ok = false;
-    for (; i < n_items; i += 2) {
+    for (; i < n_items; i += step) {
       const PItem e = i < kPItemCap ? table[i] : p_decode(a, qtiles, blockIdx.x + i * gridDim.x);
       if (e.qt * kTQ < e.nq && e.nk > 0) {
         cur.q0 = e.q0;
@@ -560,8 +560,9 @@ struct PIter {
         cur.h = e.h;
         cur.qt = e.qt;
         cur.kc = 0;
+        cur.cs = cs;
         cur.ok = true;
-        i += 2;
+        i += step;
         return;
       }
     }
@@ -576,7 +577,7 @@ struct PIter {
   }
   __device__ __forceinline__ void advance(const AttnArgs& a) {
     if (!cur.ok) return;
-    cur.kc += kTKC;
+    cur.kc += cs;
     if (cur.kc >= cur.nk) next_item(a);
   }
 };
@@ -587,7 +588,7 @@ struct PIter {
 // multiplies away.
 __device__ __forceinline__ void p_fetch_rows(const AttnArgs& a, const PUnit& un, int lane,
                                              int (&r)[16]) {
-  const int valid = min(kTKC, un.nk - un.kc);
+  const int valid = min(un.cs, un.nk - un.kc);
   const int32_t* ks = a.key_src + un.k0 + un.kc;
   const int last = __ldg(ks + valid - 1);
 #pragma unroll
@@ -603,7 +604,7 @@ __device__ __forceinline__ void p_fetch_rows(const AttnArgs& a, const PUnit& un,
 template <bool kV>
 __device__ __forceinline__ void p_gather_keys(const PMaps& mp, const PUnit& un, const int (&r)[16],
                                               uint8_t* dst, uint64_t* bar, int lane) {
-  const int ncols = (min(kTKC, un.nk - un.kc) + 15) & ~15;
+  const int ncols = (min(un.cs, un.nk - un.kc) + 15) & ~15;
   if (16 * lane >= ncols) return;
   const int col = un.h * 64;
   uint8_t* d = dst + lane * 2048;
@@ -954,6 +955,511 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 }
 
+// ----------------------------------------------------------------------------------------
+// Single-pipeline variant (astra_attention_variant 2; parity-tested, same speed as the default
+// two-pipeline kernel on ViT-B/16: 37.0 vs 37.1 us per launch, 42.0 vs 41.4 inside the step).
+// What bounds it (scripts/attn_trace_s.py, scripts/probes/pv_probe.cu): the P V MMAs
+// (13 x 128x64x16, N = head width) cost 120-185 cycles each against a 32-cycle floor, so
+// P V(u) + S(u+2) take ~1.2 us of tensor time per unit, and the softmax (MUFU-bound at
+// 16 ex2/clk/SM, softmax_probe.cu) ~1.9 us.
+// Warps 0..kSW-1 softmax (kSW/4 per TMEM lane quarter, interleaved 32-key groups), then four
+// correction warps (one per lane quarter: O readback, o = o * corr + PV, normalise + store),
+// a Q+K TMA producer, a V TMA producer and the MMA issuer.  Unit u (one 224-key chunk of one
+// 128-query tile) uses smem stage and S/P slot u%2; O has its own TMEM columns.  The MMA warp
+// issues S(u+2) right behind P V(u) (same slot, in-order tensor pipe), so the scores of the
+// next unit are ready when the softmax of this one ends, and O(u) drains during the next
+// softmax: the softmax warps (the MUFU exp2 consumers) do not wait on the tensor core.
+constexpr int kSW = 8;                     // softmax warps
+constexpr int kSHalves = kSW / 4;          // softmax warps per lane quarter
+// TMEM columns: S/P slot 0 at 0..223, O at 224..287, S/P slot 1 at 288..511
+constexpr int kSKC = 224;                  // keys per chunk
+constexpr int kSOCol = 224, kSSlot1 = 288;
+constexpr int kSProd = kSW + 4, kSProdV = kSW + 5, kSMma = kSW + 6;
+constexpr int kSThreads = (kSW + 7) * 32;
+constexpr int kSSmemUsed = 2 * kPStageBytes + 4 * 256 * 4 + 2 * 2 * 128 * 4 + 4 * 3 * 128 * 4 +
+                           512 + kPItemCap * 32 + 4 * 4096;
+constexpr int kSSmem = kSSmemUsed + 1024;
+
+struct SBars {
+  uint64_t qk_full[2], v_full[2], qk_empty[2], v_empty[2], s_full[2], p_full[2], o_full[2],
+      t_empty[2], kp_full[4], cl_full[4];
+};
+
+__device__ __forceinline__ void softmax_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kSW * 32) : "memory");
+}
+
+// P column of 32-key group g when two warps share a lane quarter: each half owns alternate
+// groups and packs a group's 32 probabilities into 16 columns of a region it already read.
+__device__ __forceinline__ int p_col2(int g) {
+  if (kSHalves == 1) return g << 4;
+  return ((g >> 2) << 6) | ((g & 1) << 5) | (((g >> 1) & 1) << 4);
+}
+
+__device__ __forceinline__ void reg_fence32(uint32_t (&r)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) asm volatile("" : "+r"(r[j]));
+}
+
+// max over the visible scores of one 32-key group
+template <bool kCausal>
+__device__ __forceinline__ float s_group_max(const uint32_t (&rr)[32], uint32_t m32, bool full) {
+  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+  if (!kCausal && full) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(rr[j]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      m4[j & 3] = fmaxf(m4[j & 3], ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY);
+  }
+  return fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+}
+
+// P = exp2(s * scale*log2e - m) of one group, packed bf16; row sum accumulated in acc
+template <bool kCausal>
+__device__ __forceinline__ void s_group_exp(const uint32_t (&rr)[32], uint32_t m32, bool full,
+                                            float2 sl2x2, float2 nm2, uint32_t (&pk)[16],
+                                            float2 (&acc)[4]) {
+  if (!kCausal && full) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const float2 t = ffma2(make_float2(__uint_as_float(rr[j]), __uint_as_float(rr[j + 1])),
+                             sl2x2, nm2);
+      const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+      pk[j >> 1] = pack_bf16x2(e.x, e.y);
+      acc[(j >> 1) & 3] = fadd2(acc[(j >> 1) & 3], e);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      const float x0 = ((m32 >> j) & 1u) ? __uint_as_float(rr[j]) : -INFINITY;
+      const float x1 = ((m32 >> (j + 1)) & 1u) ? __uint_as_float(rr[j + 1]) : -INFINITY;
+      const float2 t = ffma2(make_float2(x0, x1), sl2x2, nm2);
+      const float2 e = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+      pk[j >> 1] = pack_bf16x2(e.x, e.y);
+      acc[(j >> 1) & 3] = fadd2(acc[(j >> 1) & 3], e);
+    }
+  }
+}
+
+template <bool kCausal>
+__global__ void __launch_bounds__(kSThreads, 1)
+    attention_tcs_kernel(AttnArgs a, const __grid_constant__ PMaps mp, int qtiles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  int* sKpos = reinterpret_cast<int*>(sm + 2 * kPStageBytes);          // [4][256]
+  float* sRed = reinterpret_cast<float*>(sKpos + 4 * 256);             // [2 par][2 half][128]
+  // [4 units][corr, l half 0, l half 1][128]: 4 deep, because the softmax may run up to three
+  // units ahead of the correction warps (softmax(u+4) needs S(u+4) <- P V(u+2) <- O(u+1) read)
+  float* sCL = sRed + 2 * 2 * 128;
+  SBars* bars = reinterpret_cast<SBars*>(sCL + 4 * 3 * 128);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 1);
+  PItem* items = reinterpret_cast<PItem*>(reinterpret_cast<uint8_t*>(bars) + 512);
+  uint8_t* ostage = reinterpret_cast<uint8_t*>(items + kPItemCap);     // [4 warps][4 KB]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  long long* const trace = blockIdx.x == 0 ? g_attn_trace : nullptr;
+  if (g_attn_trace != nullptr && tid == 0) {
+    long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    g_attn_trace[512 + blockIdx.x * 2] = t0;
+  }
+  const int total = a.num_segs * a.heads * qtiles;
+  const int n_items = total > (int)blockIdx.x ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  for (int i = tid; i < min(n_items, kPItemCap); i += kSThreads)
+    items[i] = p_decode(a, qtiles, blockIdx.x + i * gridDim.x);
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars->qk_full[s], 1);
+      mbar_init(&bars->v_full[s], 1);
+      mbar_init(&bars->qk_empty[s], 1);
+      mbar_init(&bars->v_empty[s], 1);
+      mbar_init(&bars->s_full[s], 1);
+      mbar_init(&bars->p_full[s], kSW);
+      mbar_init(&bars->o_full[s], 1);
+      mbar_init(&bars->t_empty[s], 4);
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&bars->kp_full[s], 1);
+      mbar_init(&bars->cl_full[s], kSW);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kSMma) tmem_alloc<512>(tslot);
+  if (tid == kSProd * 32) {
+    tma_prefetch_desc(&mp.q);
+    tma_prefetch_desc(&mp.kl);
+    tma_prefetch_desc(&mp.vl);
+    tma_prefetch_desc(&mp.kr);
+    tma_prefetch_desc(&mp.vr);
+    tma_prefetch_desc(&mp.kl16);
+    tma_prefetch_desc(&mp.vl16);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  PIter it;
+  it.step = 1;
+  it.cs = kSKC;
+  it.init(a, qtiles, 0, items, n_items);
+
+  if (warp == kSProd || warp == kSProdV) {
+    // -------------------------------------------------------------- TMA producers (Q+K, V)
+    const bool pv = warp == kSProdV;
+    for (uint32_t u = 0; it.cur.ok; ++u, it.advance(a)) {
+      const PUnit un = it.cur;
+      const int s = u & 1;
+      const uint32_t ph = (u >> 1) & 1;
+      const int valid = min(kSKC, un.nk - un.kc), ncols = (valid + 15) & ~15;
+      uint8_t* st = sm + s * kPStageBytes;
+      int rows[16];
+      if (lane < 16) p_fetch_rows(a, un, lane, rows);
+      if (pv) {
+        mbar_wait(&bars->v_empty[s], ph ^ 1);
+        if (lane == 0) mbar_arrive_expect_tx(&bars->v_full[s], ncols * 128);
+        if (lane == 0) p_trace(trace, 5, u);
+        __syncwarp();
+        if (lane < 16)
+          p_gather_keys<true>(mp, un, rows, st + 16384 + 32768, &bars->v_full[s], lane);
+        continue;
+      }
+      int kpv[8];
+      if (kCausal) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int j = lane + 32 * m;
+          kpv[m] = j < valid ? __ldg(a.key_pos + un.k0 + un.kc + j) : 0x7FFFFFFF;
+        }
+      }
+      mbar_wait(&bars->qk_empty[s], ph ^ 1);
+      if (kCausal) {
+        // buffer u%4 was last read by the softmax of unit u-4, which ended before S(u-2)
+        // (just retired) could be issued
+        int* kp = sKpos + (u & 3) * 256;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) kp[lane + 32 * m] = kpv[m];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->kp_full[u & 3]);
+      }
+      if (lane == 0) mbar_arrive_expect_tx(&bars->qk_full[s], (128 + ncols) * 128);
+      __syncwarp();
+      if (lane == 16)
+        tma_load_2d(st, &mp.q, &bars->qk_full[s], un.h * 64, un.q0 + un.qt * kTQ, kEvictNormal);
+      if (lane < 16) p_gather_keys<false>(mp, un, rows, st + 16384, &bars->qk_full[s], lane);
+    }
+  } else if (warp == kSMma) {
+    // -------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      PIter si = it;   // S runs two units ahead of PV
+      uint32_t su = 0;
+      auto issue_s = [&]() {
+        const int s = su & 1;
+        const uint32_t ph = (su >> 1) & 1;
+        const int ncols = (min(kSKC, si.cur.nk - si.cur.kc) + 15) & ~15;
+        // slot s was last read by P V of unit su-2, issued (and so executed) before this
+        p_trace(trace, 0, su);
+        mbar_wait(&bars->qk_full[s], ph);
+        tc_fence_after();
+        p_trace(trace, 9, su);
+        const uint32_t q_s = smem_u32(sm + s * kPStageBytes), k_s = q_s + 16384;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16(tmem + s * kSSlot1, sdesc_kmajor_sw128(q_s + kk * 32),
+                   sdesc_kmajor_sw128(k_s + kk * 32), idesc_bf16_f32(128, ncols),
+                   kk > 0 ? 1u : 0u);
+        umma_commit(&bars->s_full[s]);
+        umma_commit(&bars->qk_empty[s]);
+        p_trace(trace, 1, su);
+        ++su;
+        si.advance(a);
+      };
+      if (si.cur.ok) issue_s();
+      if (si.cur.ok) issue_s();
+      for (uint32_t u = 0; it.cur.ok; ++u, it.advance(a)) {
+        const int s = u & 1;
+        const uint32_t ph = (u >> 1) & 1;
+        const int ncols = (min(kSKC, it.cur.nk - it.cur.kc) + 15) & ~15;
+        mbar_wait(&bars->p_full[s], ph);
+        p_trace(trace, 10, u);
+        mbar_wait(&bars->v_full[s], ph);
+        mbar_wait(&bars->t_empty[0], (u & 1) ^ 1);   // O(u-1) read back
+        tc_fence_after();
+        p_trace(trace, 11, u);
+        const uint32_t tS = tmem + s * kSSlot1;
+        const uint32_t v_s = smem_u32(sm + s * kPStageBytes + 16384 + 32768);
+        for (int kk = 0; kk < (ncols >> 4); ++kk)
+          umma_f16_ts(tmem + kSOCol, tS + p_col2(kk >> 1) + (kk & 1) * 8,
+                      sdesc_mnmajor_sw128(v_s + kk * 2048, 8192), idesc_bf16_f32_bmn(128, 64),
+                      kk > 0 ? 1u : 0u);
+        umma_commit(&bars->o_full[0]);
+        umma_commit(&bars->v_empty[s]);
+        p_trace(trace, 2, u);
+        if (si.cur.ok) issue_s();   // S(u+2) into the slot P V(u) just read
+      }
+    }
+  } else if (warp >= kSW) {
+    // -------------------------------------------------------------- correction warps
+    const int quarter = warp & 3, row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    uint8_t* stg = ostage + quarter * 4096;
+    float o[64];
+#pragma unroll
+    for (int d = 0; d < 64; ++d) o[d] = 0.f;
+    for (uint32_t u = 0; it.cur.ok; ++u, it.advance(a)) {
+      const PUnit un = it.cur;
+      const int s = u & 1;
+      const uint32_t ph = (u >> 1) & 1;
+      const int c4 = u & 3;
+      mbar_wait(&bars->cl_full[c4], (u >> 2) & 1);   // corr / l of this unit visible
+      const float corr = sCL[c4 * 384 + row];
+      const float l = kSHalves == 1 ? sCL[c4 * 384 + 128 + row]
+                                    : sCL[c4 * 384 + 128 + row] + sCL[c4 * 384 + 256 + row];
+      mbar_wait(&bars->o_full[0], u & 1);
+      tc_fence_after();
+      if (quarter == 0 && lane == 0) p_trace(trace, 7, u);
+      const bool rows_live = un.qt * kTQ + quarter * 32 < un.nq;
+      if (rows_live) {
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          uint32_t r0[16];
+          tmem_ld16(tmem + kSOCol + lane_off + hh * 16, r0);
+          tmem_ld_wait();
+#pragma unroll
+          for (int d = 0; d < 16; ++d) asm volatile("" : "+r"(r0[d]));
+          // corr = 0 on an item's first chunk clears what the previous item left in o
+#pragma unroll
+          for (int d = 0; d < 16; ++d)
+            o[hh * 16 + d] = fmaf(o[hh * 16 + d], corr, __uint_as_float(r0[d]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->t_empty[0]);
+      if (rows_live && un.kc + kSKC >= un.nk) {
+        const float inv = 1.0f / l;
+        // stage this warp's 32 rows x 64 dims (128 B per row, 16 B chunks XOR-swizzled by row)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4 w;
+          w.x = pack_bf16x2(o[8 * c] * inv, o[8 * c + 1] * inv);
+          w.y = pack_bf16x2(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
+          w.z = pack_bf16x2(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
+          w.w = pack_bf16x2(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+          *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) = w;
+        }
+        __syncwarp();
+        const int rbase = un.qt * kTQ + quarter * 32;
+#pragma unroll
+        for (int it2 = 0; it2 < 8; ++it2) {
+          const int r = 4 * it2 + (lane >> 3), c = lane & 7;
+          if (a.out_hi && rbase + r < un.nq)
+            *reinterpret_cast<uint4*>(a.out_hi + (size_t)(un.q0 + rbase + r) * a.ld_out +
+                                      un.h * 64 + 8 * c) =
+                *reinterpret_cast<const uint4*>(stg + r * 128 + ((c ^ (r & 7)) << 4));
+        }
+        __syncwarp();
+        const int qi = un.qt * kTQ + row;
+        if (a.out_f32 && qi < un.nq) {
+          const size_t ob = (size_t)(un.q0 + qi) * a.ld_out + un.h * 64;
+#pragma unroll
+          for (int d = 0; d < 64; ++d) a.out_f32[ob + d] = o[d] * inv;
+        }
+      }
+      if (quarter == 0 && lane == 0) p_trace(trace, 8, u);
+    }
+  } else {
+    // -------------------------------------------------------------- softmax warps
+    const int quarter = warp & 3, half = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    float m_run = -INFINITY, l_half = 0.f;
+    for (uint32_t u = 0; it.cur.ok; ++u, it.advance(a)) {
+      const PUnit un = it.cur;
+      const int s = u & 1;
+      const uint32_t ph = (u >> 1) & 1;
+      const uint32_t tS = tmem + s * kSSlot1 + lane_off;
+      const int valid = min(kSKC, un.nk - un.kc);
+      const int qi = un.qt * kTQ + row;
+      const bool warp_rows = un.qt * kTQ + quarter * 32 < un.nq;
+      const int qpos = qi < un.ncontent ? un.qpos0 + qi : 0x7FFE;
+      const int* kpos = sKpos + (u & 3) * 256;
+      if (un.kc == 0) {
+        m_run = -INFINITY;
+        l_half = 0.f;
+      }
+      if (tid == 0) p_trace(trace, 12, u);
+      if (kCausal) mbar_wait(&bars->kp_full[u & 3], (u >> 2) & 1);
+      mbar_wait(&bars->s_full[s], ph);
+      if (tid == 0) p_trace(trace, 13, u);
+      tc_fence_after();
+      if (tid == 0) p_trace(trace, 3, u);
+      // pass 1: max of keys 0..127 (groups 0-3, this half's two in one TMEM round trip).
+      // P is packed into the columns of groups 0-3 only, so the scores of keys 128.. stay in
+      // TMEM through pass 2.  The max of keys 0..127 is the exponent reference: any m with no
+      // score more than 2^64 above it gives the same softmax (P and l scale together; bf16
+      // and f32 share the exponent range).  If a later key does exceed it by more than 64
+      // (log2 units), the softmax warps vote and redo keys 128.. from their intact scores with
+      // the exact max, rescaling the P already written.
+      float mx = -INFINITY;
+      if (warp_rows && half * 32 < valid) {
+        uint32_t ra[32], rb[32];
+        const int g2 = half + kSHalves;
+        const bool two = kSHalves == 2 && g2 < 4 && g2 * 32 < valid;
+        tmem_ld32(tS + half * 32, ra);
+        if (two) tmem_ld32(tS + g2 * 32, rb);
+        const uint32_t ma = p_vis<kCausal>(kpos + half * 32, valid - half * 32, qpos);
+        const uint32_t mb = two ? p_vis<kCausal>(kpos + g2 * 32, valid - g2 * 32, qpos) : 0u;
+        tmem_ld_wait();
+        reg_fence32(ra);
+        mx = s_group_max<kCausal>(ra, ma, valid - half * 32 >= 32);
+        if (two) {
+          reg_fence32(rb);
+          mx = fmaxf(mx, s_group_max<kCausal>(rb, mb, valid - g2 * 32 >= 32));
+        }
+        if (kSHalves == 1) {   // one warp per row: groups 2, 3 as well
+          for (int g = 2; g < 4 && g * 32 < valid; ++g) {
+            tmem_ld32(tS + g * 32, ra);
+            const uint32_t m32 = p_vis<kCausal>(kpos + g * 32, valid - g * 32, qpos);
+            tmem_ld_wait();
+            reg_fence32(ra);
+            mx = fmaxf(mx, s_group_max<kCausal>(ra, m32, valid - g * 32 >= 32));
+          }
+        }
+      }
+      if (tid == 0) p_trace(trace, 14, u);
+      float cmax = mx;
+      if (kSHalves == 2) {
+        sRed[(s * 2 + half) * 128 + row] = mx;
+        softmax_bar();
+        cmax = fmaxf(sRed[s * 256 + row], sRed[s * 256 + 128 + row]);
+      }
+      if (tid == 0) p_trace(trace, 6, u);
+      float mnew = fmaxf(m_run, cmax * sl2);
+      float mref = (mnew == -INFINITY) ? 0.f : mnew;
+      // pass 2: P = exp2(s*scale*log2e - m) in bf16, into TMEM over already-read S columns
+      // (one group per load round trip: the loop is MUFU-bound, prefetching the next group
+      // measured slower — scripts/probes/softmax_probe.cu)
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                       make_float2(0.f, 0.f)};
+      float usum_lo = 0.f;   // keys 0..127
+      if (warp_rows) {
+        const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-mref, -mref);
+#pragma unroll 1
+        for (int g = half; g * 32 < valid; g += kSHalves) {
+          uint32_t rr[32], pk[16];
+          tmem_ld32(tS + g * 32, rr);
+          const uint32_t m32 = p_vis<kCausal>(kpos + g * 32, valid - g * 32, qpos);
+          tmem_ld_wait();
+          reg_fence32(rr);
+          s_group_exp<kCausal>(rr, m32, valid - g * 32 >= 32, sl2x2, nm2, pk, acc);
+          tmem_st16(tS + p_col2(g), pk);
+          if (g + kSHalves >= 4 && g < 4) {
+            const float2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+            usum_lo = (s01.x + s01.y) + (s23.x + s23.y);
+          }
+        }
+        tmem_st_wait();
+      }
+      const float2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+      float usum = (s01.x + s01.y) + (s23.x + s23.y);
+      if (valid > 128) {
+        uint32_t bad = !(usum <= 1.8446744e19f), any_bad;   // a P above 2^64, or inf / NaN
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+            "bar.red.or.pred p, 2, %2, p;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(any_bad) : "r"(bad), "n"(kSW * 32) : "memory");
+        if (any_bad) {   // rare: exact max over keys 128.., then redo them
+          float mx2 = mx;
+          if (warp_rows) {
+#pragma unroll 1
+            for (int g = 4 + ((half - 4 % kSHalves + kSHalves) % kSHalves); g * 32 < valid; g += kSHalves) {
+              uint32_t rr[32];
+              tmem_ld32(tS + g * 32, rr);
+              const uint32_t m32 = p_vis<kCausal>(kpos + g * 32, valid - g * 32, qpos);
+              tmem_ld_wait();
+              reg_fence32(rr);
+              mx2 = fmaxf(mx2, s_group_max<kCausal>(rr, m32, valid - g * 32 >= 32));
+            }
+          }
+          float cmax2 = mx2;
+          if (kSHalves == 2) {
+            __syncwarp();
+            softmax_bar();   // every half is done reading sRed of this unit
+            sRed[(s * 2 + half) * 128 + row] = mx2;
+            softmax_bar();
+            cmax2 = fmaxf(sRed[s * 256 + row], sRed[s * 256 + 128 + row]);
+          }
+          const float mnew2 = fmaxf(m_run, cmax2 * sl2);
+          const float mref2 = (mnew2 == -INFINITY) ? 0.f : mnew2;
+          const float resc = ex2_approx(mref - mref2);
+          usum = usum_lo * resc;
+          if (warp_rows) {
+            // rescale the P of keys 0..127
+#pragma unroll 1
+            for (int g = half; g < 4 && g * 32 < valid; g += kSHalves) {
+              uint32_t pk[16];
+              tmem_ld16(tS + p_col2(g), pk);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float lo = __uint_as_float(pk[j] << 16), hi = __uint_as_float(pk[j] & 0xFFFF0000u);
+                pk[j] = pack_bf16x2(lo * resc, hi * resc);
+              }
+              tmem_st16(tS + p_col2(g), pk);
+            }
+            // recompute keys 128..
+            float2 acc2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                              make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-mref2, -mref2);
+#pragma unroll 1
+            for (int g = 4 + ((half - 4 % kSHalves + kSHalves) % kSHalves); g * 32 < valid; g += kSHalves) {
+              uint32_t rr[32], pk[16];
+              tmem_ld32(tS + g * 32, rr);
+              const uint32_t m32 = p_vis<kCausal>(kpos + g * 32, valid - g * 32, qpos);
+              tmem_ld_wait();
+              reg_fence32(rr);
+              s_group_exp<kCausal>(rr, m32, valid - g * 32 >= 32, sl2x2, nm2, pk, acc2);
+              tmem_st16(tS + p_col2(g), pk);
+            }
+            tmem_st_wait();
+            const float2 t01 = fadd2(acc2[0], acc2[1]), t23 = fadd2(acc2[2], acc2[3]);
+            usum += (t01.x + t01.y) + (t23.x + t23.y);
+          }
+          mnew = mnew2;
+        }
+      }
+      const float corr = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - mnew);
+      l_half = l_half * corr + usum;
+      m_run = mnew;
+      if (half == 0) sCL[(u & 3) * 384 + row] = corr;
+      sCL[(u & 3) * 384 + 128 + half * 128 + row] = l_half;
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bars->p_full[s]);
+        mbar_arrive(&bars->cl_full[u & 3]);
+      }
+      if (tid == 0) p_trace(trace, 4, u);
+
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (g_attn_trace != nullptr && tid == 0) {
+    long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    g_attn_trace[512 + blockIdx.x * 2 + 1] = t1;
+  }
+  if (warp == kSMma) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 template <int DH>
 static int launch_attn(const AttnArgs& a, dim3 grid, cudaStream_t st) {
   constexpr int smem = 2 * kAK * (DH + 1) * 4 + kAQ * (kAK + 1) * 4 + kAK * 4;
@@ -1008,10 +1514,14 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
       ASTRA_CUDA_CHECK(cudaFuncSetAttribute(attention_tcp_kernel<true>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmem));
+      ASTRA_CUDA_CHECK(cudaFuncSetAttribute(attention_tcs_kernel<false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem));
+      ASTRA_CUDA_CHECK(cudaFuncSetAttribute(attention_tcs_kernel<true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kSSmem));
       configured = true;
     }
     const int qtiles = (max_nq + kTQ - 1) / kTQ;
-    if (g_attention_variant == 0) {
+    if (g_attention_variant != 1) {
       const long items = (long)num_segs * heads * qtiles;
       const int grid = (int)std::min<long>(items, num_sms());
       // gather maps (SW128, true row extents: boxes running past a buffer are zero-filled)
@@ -1028,10 +1538,16 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
           (rc = make_tmap_2d(&mp.kr, k_remote, bf, 2, rr, ld_remote, ld_remote, 1, 64, true)) ||
           (rc = make_tmap_2d(&mp.vr, v_remote, bf, 2, rr, ld_remote, ld_remote, 1, 64, true)))
         return rc;
-      if (causal)
+      if (g_attention_variant == 2) {
+        if (causal)
+          attention_tcs_kernel<true><<<grid, kSThreads, kSSmem, st>>>(a, mp, qtiles);
+        else
+          attention_tcs_kernel<false><<<grid, kSThreads, kSSmem, st>>>(a, mp, qtiles);
+      } else if (causal) {
         attention_tcp_kernel<true><<<grid, kPThreads, kPSmem, st>>>(a, mp, qtiles);
-      else
+      } else {
         attention_tcp_kernel<false><<<grid, kPThreads, kPSmem, st>>>(a, mp, qtiles);
+      }
     } else {
       dim3 tgrid(num_segs, heads, qtiles);
       attention_tc_kernel<<<tgrid, kTcThreads, kTcSmem, st>>>(a);

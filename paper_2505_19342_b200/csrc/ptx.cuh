@@ -360,6 +360,22 @@ ASTRA_DEVICE float2 fadd2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+// 2^x for a pair on the FMA pipe, leaving the MUFU free: x = n + f by round-to-nearest
+// (magic-number add), f in [-0.5, 0.5]; degree-3 fit of 2^f (max rel. error 1.0e-4, below the
+// bf16 rounding of P); n added to the exponent field.  x is clamped at -126 (masked scores give
+// 2^-126, not 0).
+ASTRA_DEVICE float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);
+  float2 q = ffma2(f, make_float2(0.05500893f, 0.05500893f), make_float2(0.242211f, 0.242211f));
+  q = ffma2(f, q, make_float2(0.69328293f, 0.69328293f));
+  q = ffma2(f, q, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
 ASTRA_DEVICE float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

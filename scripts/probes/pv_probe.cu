@@ -1,0 +1,128 @@
+// Probe: rate of the attention P.V MMAs (13 x tcgen05.mma 128x64x16, A = P from TMEM or smem,
+// B = V MN-major SW128 in smem) alone and while 8 warps run the softmax TMEM ld/exp/st loop.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../../paper_2505_19342_b200/csrc -o pv_probe pv_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "ptx.cuh"
+using namespace astra;
+
+__host__ __device__ constexpr uint32_t idesc_bmn(uint32_t M, uint32_t N) {
+  return idesc_bf16_f32(M, N) | (1u << 16);
+}
+
+// mode bit0: softmax traffic on; bit1: A from smem (SS) instead of TMEM (TS); bit2: S MMA (N=208, K=64 SS)
+__global__ void __launch_bounds__(288, 1) k(long long* out, int batches, int mode) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t slot;
+  __shared__ uint64_t bar;
+  __shared__ int stop;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3f803f80u;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); stop = 0; fence_barrier_init(); }
+  if (warp == 8) tmem_alloc<512>(&slot);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (warp == 8) {
+    if (lane == 0) {
+      const uint32_t v_s = smem_u32(sm), a_s = smem_u32(sm + 65536);
+      long long t0 = clock64();
+      int nw = 0;
+      for (int b = 0; b < batches; ++b) {
+        if (mode >= 128) {   // 13 SS MMAs 128 x N x 16, K-major A and B, N = mode - 128
+          const int N = mode - 128;
+          for (int kk = 0; kk < 13; ++kk)
+            umma_f16(tmem + 256, sdesc_kmajor_sw128(a_s + (kk & 3) * 32), sdesc_kmajor_sw128(v_s + (kk & 3) * 32),
+                     idesc_bf16_f32(128, N), kk > 0);
+        } else if (mode & 4) {
+          for (int kk = 0; kk < 4; ++kk)
+            umma_f16(tmem + 256, sdesc_kmajor_sw128(a_s + kk * 32), sdesc_kmajor_sw128(v_s + kk * 32),
+                     idesc_bf16_f32(128, 208), kk > 0);
+        } else {
+          for (int kk = 0; kk < 13; ++kk) {
+            if (mode & 2)
+              umma_f16(tmem + 384, sdesc_kmajor_sw128(a_s + (kk >> 2) * 16384 + (kk & 3) * 32),
+                       sdesc_mnmajor_sw128(v_s + kk * 2048, 8192), idesc_bmn(128, 64), kk > 0);
+            else if (mode & 8)   // two independent accumulators
+              umma_f16_ts(tmem + 384 + (kk & 1) * 64, tmem + 256 + kk * 8, sdesc_mnmajor_sw128(v_s + kk * 2048, 8192),
+                          idesc_bmn(128, 64), kk > 1);
+            else if (mode & 16)  // four independent accumulators
+              umma_f16_ts((kk & 3) * 64 + ((kk & 3) >= 2 ? 256 : 0) + tmem, tmem + 256 + kk * 8, sdesc_mnmajor_sw128(v_s + kk * 2048, 8192),
+                          idesc_bmn(128, 64), kk > 3);
+            else if (mode & 32)  // K-major B (V^T) instead of MN-major
+              umma_f16_ts(tmem + 384, tmem + 256 + kk * 8, sdesc_kmajor_sw128(v_s + (kk >> 2) * 8192 + (kk & 3) * 32),
+                          idesc_bf16_f32(128, 64), kk > 0);
+            else
+              umma_f16_ts(tmem + 384, tmem + 256 + kk * 8, sdesc_mnmajor_sw128(v_s + kk * 2048, 8192),
+                          idesc_bmn(128, 64), kk > 0);
+          }
+        }
+        if ((mode & 64) == 0 || mode >= 128 || (b & 7) == 7) {
+          umma_commit(&bar);
+          mbar_wait_spin(&bar, nw & 1);
+          ++nw;
+        }
+      }
+      long long t1 = clock64();
+      out[blockIdx.x] = (t1 - t0) / batches;
+      stop = 1;
+    }
+  } else if (mode & 1) {
+    const uint32_t t = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const int half = warp >> 2;
+    float2 acc = make_float2(0.f, 0.f);
+    const float2 sl = make_float2(0.18f, 0.18f), nm = make_float2(-1.f, -1.f);
+    while (!*(volatile int*)&stop) {
+      for (int g = half; g < 7; g += 2) {
+        uint32_t r[32], pk[16];
+        tmem_ld32(t + g * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) asm volatile("" : "+r"(r[j]));
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float2 x = ffma2(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sl, nm);
+          const float2 e = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          pk[j >> 1] = pack_bf16x2(e.x, e.y);
+          acc = fadd2(acc, e);
+        }
+        tmem_st16(t + g * 16, pk);
+      }
+      tmem_st_wait();
+    }
+    if (acc.x == 1.2345f) out[1000 + threadIdx.x] = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) { tc_fence_after(); tmem_dealloc<512>(tmem); }
+}
+
+int main() {
+  long long* o; cudaMalloc(&o, 4096 * 8);
+  const int smem = 160 * 1024 + 1024;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const char* names[] = {"PV TS alone", "PV TS + softmax", "PV SS alone", "PV SS + softmax",
+                         "S 128x208x64 alone", "S + softmax", "PV TS 2 accum", "PV TS 4 accum", "PV TS Kmajor B",
+                         "PV TS no-wait", "PV SS no-wait", "S no-wait", "PV TS no-wait +sm"};
+  const int modes[] = {0, 1, 2, 3, 4, 5, 8, 16, 32, 64, 66, 68, 65};
+  for (int N : {16, 32, 64, 128, 256}) {
+    k<<<148, 288, smem>>>(o, 2000, 128 + N);
+    cudaDeviceSynchronize();
+    long long h;
+    cudaMemcpy(&h, o, 8, cudaMemcpyDeviceToHost);
+    printf("13 x SS 128x%dx16 (commit+wait per batch): %lld cycles\n", N, h);
+  }
+  for (int m = 9; m < 13; ++m) {
+    k<<<148, 288, smem>>>(o, 2000, modes[m]);
+    k<<<148, 288, smem>>>(o, 2000, modes[m]);
+    cudaDeviceSynchronize();
+    long long h;
+    cudaMemcpy(&h, o, 8, cudaMemcpyDeviceToHost);
+    printf("%-22s %lld cycles per batch (floor: PV 13x32 = 416, S 4x104 = 416)\n", names[m], h);
+  }
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
