@@ -238,6 +238,12 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                 "astra_gemm: passes=3 needs lo operands");
   ASTRA_REQUIRE(out_lo == nullptr || out_hi != nullptr, ASTRA_ERR_SHAPE,
                 "astra_gemm: out_lo requires out_hi");
+  static int debug_set = -1;
+  if (debug_set < 0) {   // bench-only isolation switch, see tc_gemm.cuh
+    const char* d = getenv("ASTRA_GEMM_DEBUG");
+    debug_set = d ? atoi(d) : 0;
+    if (debug_set) ASTRA_CUDA_CHECK(cudaMemcpyToSymbol(g_gemm_debug, &debug_set, sizeof(int)));
+  }
   int BN, cluster;
   pick_tile(M, N, &BN, &cluster);
   if (const char* f = getenv("ASTRA_GEMM_BN")) {   // A/B hook (benchmarks)

@@ -95,6 +95,11 @@ struct TileSched {
 // tensor pipe.  Barriers: the leader's full barrier counts both CTAs' TMA bytes; its MMA
 // commits (multicast) release the stage / publish the accumulator in both CTAs; both CTAs'
 // epilogue warps arrive on the leader's TMEM-empty barrier.
+// Bench-only isolation switch (ASTRA_GEMM_DEBUG, gemm.cu): bit 0 skips the UMMAs (stages are
+// still consumed and released), bit 1 skips the epilogue work, bit 2 skips the TMA loads.
+// 0 in production.
+static __device__ int g_gemm_debug = 0;
+
 template <int BN, int PASSES, int STAGES, int CLUSTER, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
@@ -172,7 +177,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * S::kStageBytes;
           const int kc = kb * kBK;
-          if (kQuad) {
+          if (g_gemm_debug & 4) {   // no loads: the stage is "full" at once (MMA on stale data)
+            if (leader) mbar_arrive(&full_bar[stage]);
+          } else if (kQuad) {
             // this CTA's half of the A tile goes to both pairs; B half to itself
             if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * S::kStageBytes);
             const uint32_t fb = full_pb + stage * 8, fl = full0 + stage * 8;
@@ -233,6 +240,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t a_lo = st + S::kATile + S::kBTile, b_lo = st + 2 * S::kATile + S::kBTile;
 #pragma unroll
           for (int kk = 0; kk < kBK / kUK; ++kk) {
+            if (g_gemm_debug & 1) break;
             const uint32_t koff = kk * kUK * 2;  // bytes inside the 128B swizzle row
             const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
             if (kPair) {
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;
-      epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage);
+      if (!(g_gemm_debug & 2)) epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage);
       tc_fence_before();
       if (kPair) {
         __syncwarp();
