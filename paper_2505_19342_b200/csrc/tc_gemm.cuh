@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  const int dbg = g_gemm_debug;   // read once: the loops below clobber memory
   const int rank = kPair ? (int)cluster_ctarank() : 0;
   const bool leader = (rank & 1) == 0;   // issues the pair's UMMAs
   const int pair_leader = rank & ~1;
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * S::kStageBytes;
           const int kc = kb * kBK;
-          if (g_gemm_debug & 4) {   // no loads: the stage is "full" at once (MMA on stale data)
+          if (dbg & 4) {   // no loads: the stage is "full" at once (MMA on stale data)
             if (leader) mbar_arrive(&full_bar[stage]);
           } else if (kQuad) {
             // this CTA's half of the A tile goes to both pairs; B half to itself
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t a_lo = st + S::kATile + S::kBTile, b_lo = st + 2 * S::kATile + S::kBTile;
 #pragma unroll
           for (int kk = 0; kk < kBK / kUK; ++kk) {
-            if (g_gemm_debug & 1) break;
+            if (dbg & 1) break;
             const uint32_t koff = kk * kUK * 2;  // bytes inside the 128B swizzle row
             const uint32_t accum = (kb > 0 || kk > 0) ? 1u : 0u;
             if (kPair) {
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;
-      if (!(g_gemm_debug & 2)) epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage);
+      if (!(dbg & 2)) epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage);
       tc_fence_before();
       if (kPair) {
         __syncwarp();
