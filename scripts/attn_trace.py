@@ -8,7 +8,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2505_19342_b200 import _native, cluster, data, model, vq  # noqa: E402
-from paper_2505_19342_b200.runtime import AstraRuntime  # noqa: E402
+from paper_2505_19342_b200.runtime import AstraRuntime, LoopbackExchange  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 cfg = model.ModelConfig(layers=1, hidden=768, heads=12, vocab_or_classes=1000, max_tokens=197,
@@ -19,7 +19,8 @@ rng = np.random.default_rng(0)
 for i, b in enumerate(params.blocks):
     c = xs.reshape(-1, 768)[rng.choice(64 * 196, 1024, replace=False)]
     b.codebook = vq.Codebook(layer_id=i, groups=1, centroids=[c])
-rt = AstraRuntime(params, cluster.partition_tokens(196, n), batch=64, precision="fast")
+comm = LoopbackExchange(n - 1, n) if n > 1 else None   # one rank (the last) of an N-way split
+rt = AstraRuntime(params, cluster.partition_tokens(196, n), batch=64, precision="fast", comm=comm)
 rt.stage_input(xs)
 rt.forward()
 torch.cuda.synchronize()

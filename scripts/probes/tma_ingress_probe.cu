@@ -102,6 +102,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64, 1)
   if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) / (it ? it : 1);
 }
 
+
+// 16 lanes of one warp each issue a 16-row box per stage (the attention producer's pattern)
+__global__ void __launch_bounds__(64, 1) k16(const __grid_constant__ CUtensorMap map, int stages, int loads,
+                                             int lanes, int row_blocks, int col_blocks, long long* out) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[16], empty[16];
+  const int lane = threadIdx.x & 31;
+  const int bytes = lanes * 2048;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  long long t0 = clock64();
+  if (threadIdx.x < 32) {
+    for (int i = 0; i < loads; ++i) {
+      const int s = i % stages;
+      const uint32_t ph = (i / stages) & 1;
+      mbar_wait(&empty[s], ph ^ 1);
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
+      __syncwarp();
+      if (lane < lanes) {
+        const int t = (blockIdx.x + i * gridDim.x) * lanes + lane;
+        tma_load_2d(sm + s * bytes + lane * 2048, &map, &full[s], (t / row_blocks) % col_blocks * 64,
+                    (t % row_blocks) * 16, 0x1000000000000000ull);
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    for (int i = 0; i < loads; ++i) {
+      const int s = i % stages;
+      mbar_wait(&full[s], (i / stages) & 1);
+      mbar_arrive(&empty[s]);
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -128,7 +168,7 @@ int main() {
     enc(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B, gb, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     cudaFuncSetAttribute(kpair, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    for (int mode = 0; mode < 2; ++mode)
+    for (int mode = 0; mode < 0; ++mode)
       for (int stages : {3, 4, 5, 6}) {
         for (int rep = 0; rep < 2; ++rep)
           kpair<<<148, 64, stages * 32768 + 1024>>>(ma, mb, stages, 12, 12608 / 256, 2304 / 256, mode, out);
@@ -139,8 +179,29 @@ int main() {
                mode ? "per-CTA barriers" : "pair loads", stages, avg, 32768.0 / avg);
       }
   }
+
+  {
+    CUtensorMap map;
+    cuuint64_t gdim[2] = {cols, 4096};
+    cuuint64_t gstr[1] = {cols * 2};
+    cuuint32_t box[2] = {64, 16};
+    cuuint32_t es[2] = {1, 1};
+    enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cudaFuncSetAttribute(k16, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int lanes : {1, 4, 16}) {
+      const int stages = 4, loads = 400;
+      for (int rep = 0; rep < 2; ++rep)
+        k16<<<148, 64, stages * lanes * 2048 + 1024>>>(map, stages, loads, lanes, 4096 / 16, cols / 64, out);
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, out, 148 * 8, cudaMemcpyDeviceToHost);
+      double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i] / 148.0;
+      printf("16-row boxes, %2d lanes issuing per step: %.0f clk per box, %.1f B/clk/SM\n", lanes,
+             avg / (loads * lanes), (double)loads * lanes * 2048 / avg);
+    }
+  }
   for (int use_rows : {4096}) {      // 24 MB (L2-resident) / 384 MB (HBM)
-    for (int box_rows : {64, 128, 256}) {
+    for (int box_rows : {16}) {
       CUtensorMap map;
       cuuint64_t gdim[2] = {cols, (cuuint64_t)use_rows};
       cuuint64_t gstr[1] = {cols * 2};
@@ -148,10 +209,10 @@ int main() {
       cuuint32_t es[2] = {1, 1};
       enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      for (int stages : {2, 4, 6, 8, 12}) {
+      for (int stages : {4, 8, 16}) {
         const int bytes = box_rows * 128;
         if (stages * bytes > 190 * 1024) continue;
-        const int loads = (64 << 20) / bytes / 148 * 4;   // ~256 MB total
+        const int loads = bytes >= 8192 ? (64 << 20) / bytes / 148 * 4 : 2000;
         for (int rep = 0; rep < 2; ++rep)
           k<<<148, 64, stages * bytes + 1024>>>(map, stages, box_rows, loads, use_rows / box_rows, cols / 64, out);
         cudaDeviceSynchronize();
