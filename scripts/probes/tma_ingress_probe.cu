@@ -190,7 +190,7 @@ int main() {
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     cudaFuncSetAttribute(k16, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     for (int lanes : {1, 4, 16, 32}) {
-      const int stages = 4, loads = 400;
+      const int stages = lanes == 32 ? 2 : 4, loads = 400;
       for (int rep = 0; rep < 2; ++rep)
         k16<<<148, 64, stages * lanes * 2048 + 1024>>>(map, stages, loads, lanes, 4096 / 16, cols / 64, out);
       cudaDeviceSynchronize();
