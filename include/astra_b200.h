@@ -210,7 +210,8 @@ int astra_attention_masked(const float* q, const float* k, const float* v, int R
 /* Route astra_attention to the fp32 SIMT kernel even when the tcgen05 bf16
  * kernel applies (test / A-B hook). */
 int astra_attention_force_simt(int enable);
-/* Test hook: tcgen05 variant — 0 persistent warp-specialised (default), 1 one CTA per tile. */
+/* Test hook: tcgen05 variant — 0 persistent two-pipeline (default), 1 one CTA per tile,
+   2 persistent single pipeline with correction warps (attention_tcs_kernel). */
 int astra_attention_variant(int variant);
 /* Debug hook: CTA 0 of the persistent kernel writes per-unit globaltimer stamps
  * (int64 [64][8]) to buf; NULL disables. */
