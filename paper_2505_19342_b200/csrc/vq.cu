@@ -381,11 +381,16 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       const int src = rows ? rows[row] : row;
       const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
       const float* cents = cb.centroids + (size_t)g * K * gd;
-      float xs[32];
+      // the token slice and the first candidate pair load in the same round trip
+      float xs[32], c0[32], c1[32];
+      int k0 = __shfl_sync(0xffffffffu, ev, 2);
+      int k1 = nd > 1 ? __shfl_sync(0xffffffffu, ev, 3) : k0;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const int e = lane + 32 * i;
         xs[i] = e < gd ? __ldg(xr + e) : 0.0f;
+        c0[i] = e < gd ? __ldg(cents + (size_t)k0 * gd + e) : 0.0f;
+        c1[i] = e < gd ? __ldg(cents + (size_t)k1 * gd + e) : 0.0f;
       }
       double pp = 0.0;
 #pragma unroll
@@ -394,16 +399,15 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       double bd = INFINITY;
       int bi = -1;
       for (int q = 0; q < nd; q += 2) {
-        const int k0 = __shfl_sync(0xffffffffu, ev, 2 + q);
-        const int k1 = q + 1 < nd ? __shfl_sync(0xffffffffu, ev, 3 + q) : k0;
-        const float* c0p = cents + (size_t)k0 * gd;
-        const float* c1p = cents + (size_t)k1 * gd;
-        float c0[32], c1[32];
+        if (q > 0) {
+          k0 = __shfl_sync(0xffffffffu, ev, 2 + q);
+          k1 = q + 1 < nd ? __shfl_sync(0xffffffffu, ev, 3 + q) : k0;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int e = lane + 32 * i;
-          c0[i] = e < gd ? __ldg(c0p + e) : 0.0f;
-          c1[i] = e < gd ? __ldg(c1p + e) : 0.0f;
+          for (int i = 0; i < 32; ++i) {
+            const int e = lane + 32 * i;
+            c0[i] = e < gd ? __ldg(cents + (size_t)k0 * gd + e) : 0.0f;
+            c1[i] = e < gd ? __ldg(cents + (size_t)k1 * gd + e) : 0.0f;
+          }
         }
         const double cc0 = cb.c_sq64[(size_t)g * K + k0], cc1 = cb.c_sq64[(size_t)g * K + k1];
         double d0 = 0.0, d1 = 0.0;
