@@ -176,6 +176,9 @@ struct VqEpilogue {
     // (columns >= K get +inf, so they never win and never enter the window)
     float* scs = reinterpret_cast<float*>(stage);
     const int lane = threadIdx.x & 31;
+    // the re-rank list count for the finalize kernel that follows (stream order): reset by
+    // one thread here instead of a memset node in front of this GEMM
+    if (tc.m_blk == 0 && tc.n_blk == 0 && g == 0 && row_in_tile == 0 && cb == 0) *w.rr_count = 0;
     float bst[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
 #pragma unroll 1
     for (int c0 = cb; c0 < ce; c0 += 32) {
@@ -653,6 +656,7 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
                             const int32_t* rows, int rec_by_row, int32_t* idx_out, int32_t* stats,
                             cudaStream_t s) {
   const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
+  if (Mg <= 0 || M <= 0) return ASTRA_OK;   // (the GEMM's tile (0, 0) resets the re-rank count)
   const int cluster = (Mg > kBM) ? 2 : 1;  // CTA pairs split the codebook tile (cta_group::2)
   const long units256 = (long)G * ((Mg + kBM * cluster - 1) / (kBM * cluster)) * ((K + kVqBN - 1) / kVqBN);
   const int bn = (units256 * 2 * cluster <= num_sms()) ? kVqBNMin : kVqBN;
@@ -669,7 +673,6 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
                                     : vq_launch_gemm<kVqBNMin>(cb, ta, talo, Mg, w, nchunk, cluster, s);
   ASTRA_CUDA_CHECK(e);
   const int items = G * M;
-  ASTRA_CUDA_CHECK(cudaMemsetAsync(w.rr_count, 0, sizeof(int), s));
   vq_finalize_kernel<<<(items + 7) / 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                       stats, Mg, rec_by_row);
   ASTRA_CUDA_CHECK(cudaGetLastError());
