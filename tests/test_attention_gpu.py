@@ -126,13 +126,16 @@ def test_attention_kernels_vs_torch(cuda, spec, causal, force_simt, variant):
     assert err < tol, err
 
 
+@pytest.mark.parametrize("variant", [0, 2])
 @pytest.mark.parametrize("factor", [8.0, 60.0])
 @pytest.mark.parametrize("causal", [False, True])
-def test_attention_score_outliers(cuda, factor, causal):
-    """Keys whose scores sit far above the first keys of the row: the tcgen05 kernel's
-    exponent reference (first-group estimate) must either absorb them (P up to 2^64) or fall
-    back to the exact row max."""
+def test_attention_score_outliers(cuda, factor, causal, variant):
+    """Keys whose scores sit far above the first keys of the row.  The single-pipeline kernel
+    (variant 2) takes its exponent reference from keys 0..127 and must either absorb them
+    (P up to 2^64) or redo keys 128.. with the exact row max; the default kernel uses the
+    exact max throughout."""
     from paper_2505_19342_b200 import _native
+    _native.load().astra_attention_variant(variant)
     heads, dk = 12, 64
     spec = [(197, 197, 1), (50, 300, 0)]
     qkv, table, segs_t, ks, kp, segs = _problem(11, spec, heads, dk, causal)
@@ -155,6 +158,7 @@ def test_attention_score_outliers(cuda, factor, causal):
                  qkv.shape[0], qkv.shape[0], table.shape[0],
                  torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
+    _native.load().astra_attention_variant(0)
     ref = _reference(qkv, table, segs, ks, kp, heads, dk, causal)
     rows = torch.cat([torch.arange(s[0], s[0] + s[1]) for s in segs]).cuda()
     o = out.float()[rows]
