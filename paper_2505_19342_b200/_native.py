@@ -110,7 +110,7 @@ def check(status: int, what: str = "") -> None:
 
 
 # kernels each C-ABI call enqueues (for launch accounting in bench.py)
-LAUNCHES = {"astra_vq_encode": 3, "astra_vq_prepare": 2, "astra_vq_encode_split": 2}
+LAUNCHES = {"astra_vq_encode": 3, "astra_vq_prepare": 2, "astra_vq_encode_split": 3}
 _counter: dict | None = None
 
 
