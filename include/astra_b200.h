@@ -186,6 +186,14 @@ int astra_argmax_rows(const float* logits, int rows, int cols, int ld, int32_t* 
                       void* stream);
 int astra_decode_advance(int32_t* pos, int32_t* segs, int rows, void* stream);
 
+/* Codebook setup (replaces the centroid update of vq._lloyd, vq.py:160-165, and the
+ * per-cluster sums of kmeans_init, vq.py:190-192): mean[c] = sum of pts[order[i]] for
+ * i in [seg[c], seg[c+1]) in ascending order, / count — fp64, bit-identical to NumPy's
+ * axis-0 mean for the same assignment.  Empty clusters leave mean[c] untouched; sums
+ * (optional) receives every cluster's sum. */
+int astra_segment_mean_f64(const double* pts, int ld, const int32_t* order, const int32_t* seg,
+                           int k, int dim, double* mean, double* sums, void* stream);
+
 /* --------------------------------------------------- mixed-precision attention
  * attention.multihead_attention + tensor.masked_softmax (attention.py:50-73,
  * tensor.py:295-315) over each device's mixed key set (cluster.py:201-212).

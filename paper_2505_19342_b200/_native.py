@@ -56,6 +56,7 @@ SIGNATURES: dict[str, list] = {
     "astra_append_kv": [_vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp],
     "astra_argmax_rows": [_vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _c_int, _vp, _vp],
     "astra_decode_advance": [_vp, _vp, _c_int, _vp],
+    "astra_segment_mean_f64": [_vp, _c_int, _vp, _vp, _c_int, _c_int, _vp, _vp, _vp],
     "astra_attention_masked": [_vp, _vp, _vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
                                _vp],
 }

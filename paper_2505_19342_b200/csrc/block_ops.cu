@@ -232,7 +232,16 @@ __global__ void append_kv_kernel(const uint8_t* __restrict__ k_new, const uint8_
   warp_copy16(dst + row_bytes, v_new + (size_t)b * ld_new, row_bytes, lane);
 }
 
-// greedy argmax per row, lowest index on ties (np.argmax, model.py:358 / cluster.py:302)
+// np.argmax order (model.py:358 / cluster.py:302): NaN ranks above every number (the first
+// NaN wins), then the larger value, then the lower index on ties.  An all -inf row picks 0.
+__device__ __forceinline__ bool argmax_better(float v, int i, float bv, int bi) {
+  const bool vn = isnan(v), bn = isnan(bv);
+  if (vn != bn) return vn;
+  if (vn) return i < bi;
+  return v > bv || (v == bv && i < bi);
+}
+
+// greedy argmax per row, lowest index on ties
 __global__ void argmax_rows_kernel(const float* __restrict__ logits, int cols, int ld,
                                    int32_t* __restrict__ out, int out_stride,
                                    const int32_t* __restrict__ step_pos, int pos_base,
@@ -243,7 +252,7 @@ __global__ void argmax_rows_kernel(const float* __restrict__ logits, int cols, i
   int bi = 0x7FFFFFFF;
   for (int c = threadIdx.x; c < cols; c += blockDim.x) {
     const float v = lr[c];
-    if (v > bv) {  // strictly greater: the first (lowest) index of a tie stays
+    if (argmax_better(v, c, bv, bi)) {
       bv = v;
       bi = c;
     }
@@ -251,7 +260,7 @@ __global__ void argmax_rows_kernel(const float* __restrict__ logits, int cols, i
   for (int o = 16; o; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) {
+    if (argmax_better(ov, oi, bv, bi)) {
       bv = ov;
       bi = oi;
     }
@@ -266,10 +275,11 @@ __global__ void argmax_rows_kernel(const float* __restrict__ logits, int cols, i
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
-      if (sv[i] > bv || (sv[i] == bv && si[i] < bi)) {
+      if (argmax_better(sv[i], si[i], bv, bi)) {
         bv = sv[i];
         bi = si[i];
       }
+    if (bi == 0x7FFFFFFF) bi = 0;   // cols == 0 cannot happen; keep the id in range anyway
     const int slot = step_pos ? step_pos[row] - pos_base : 0;
     out[(size_t)row * out_stride + slot] = bi;
     if (next_tok) next_tok[row] = bi;
@@ -295,6 +305,25 @@ static int grid_rows(int rows, int warps_per_block) {
 }  // namespace astra
 
 using namespace astra;
+
+// Lloyd centroid update (vq.py:160-165 `pts[assign == k].mean(axis=0)`): thread per
+// (cluster, dim) sums its cluster's points in ascending sample order in fp64 — NumPy's
+// axis-0 reduction order — then divides by the count, so the result is bit-identical to the
+// reference's mean for the same assignment.  `order` lists the sample ids sorted by cluster
+// (stable), seg[k]..seg[k+1] the range of cluster k.  Empty clusters keep `mean` unchanged.
+__global__ void segment_mean_f64_kernel(const double* __restrict__ pts, int ld,
+                                        const int32_t* __restrict__ order,
+                                        const int32_t* __restrict__ seg, int k, int dim,
+                                        double* __restrict__ mean, double* __restrict__ sums) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (d >= dim || c >= k) return;
+  const int s0 = seg[c], s1 = seg[c + 1];
+  double acc = 0.0;
+  for (int i = s0; i < s1; ++i) acc += pts[(size_t)order[i] * ld + d];
+  if (sums) sums[(size_t)c * dim + d] = acc;
+  if (s1 > s0) mean[(size_t)c * dim + d] = acc / (double)(s1 - s0);
+}
 
 extern "C" int astra_layernorm_ex(const float* x, int M, int D, int ldx, const float* gain,
                                   const float* bias, float eps, float* out_f32, int ld_f32,
@@ -461,6 +490,18 @@ extern "C" int astra_argmax_rows(const float* logits, int rows, int cols, int ld
 extern "C" int astra_decode_advance(int32_t* pos, int32_t* segs, int rows, void* stream) {
   if (rows == 0) return ASTRA_OK;
   decode_advance_kernel<<<(rows + 127) / 128, 128, 0, as_stream(stream)>>>(pos, segs, rows);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_segment_mean_f64(const double* pts, int ld, const int32_t* order,
+                                      const int32_t* seg, int k, int dim, double* mean,
+                                      double* sums, void* stream) {
+  ASTRA_REQUIRE(k >= 0 && dim >= 0 && ld >= dim, ASTRA_ERR_SHAPE, "segment_mean: bad shape");
+  if (k == 0 || dim == 0) return ASTRA_OK;
+  dim3 grid((dim + 127) / 128, k);
+  segment_mean_f64_kernel<<<grid, 128, 0, as_stream(stream)>>>(pts, ld, order, seg, k, dim, mean,
+                                                              sums);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }

@@ -32,7 +32,7 @@ import numpy as np
 import torch
 
 from . import _native, kernels
-from .errors import ShapeError
+from .errors import IndexCorruptionError, LifecycleError, ShapeError
 from .layout import sp_layout
 from .model import LN_EPS, class_owner_ids
 from .vq import DeviceCodebook, index_bits
@@ -48,6 +48,20 @@ def _p(t: torch.Tensor | None, elem_offset: int = 0) -> int | None:
     if t is None:
         return None
     return t.data_ptr() + elem_offset * t.element_size()
+
+
+def _check_fp32(params) -> None:
+    """The runtime keeps the reference's fp32 storage (tensor.py:26-31); an fp64 model would
+    silently lose precision here, so it is rejected instead."""
+    for name, t in params.named_tensors():
+        dt = np.asarray(t.data).dtype
+        if dt != np.float32:
+            raise ShapeError(f"{name}: the B200 runtime stores fp32 parameters, got {dt}")
+    for b in params.blocks:
+        if b.codebook is not None:
+            for c in b.codebook.centroids:
+                if np.asarray(c).dtype != np.float32:
+                    raise ShapeError("codebook centroids must be fp32 for the B200 runtime")
 
 
 class TorchDistExchange:
@@ -99,7 +113,7 @@ class AstraRuntime:
     def __init__(self, params, plan, batch: int, mode: str = "classify",
                  cls_mode: str = "distributed", precision: str = "parity", comm=None,
                  device: torch.device | None = None, encode_at_one_device: bool = True,
-                 require_codebooks: bool = True):
+                 require_codebooks: bool = True, sync_params: bool = True):
         if precision not in ("parity", "fast"):
             raise ValueError("precision must be 'parity' or 'fast'")
         if not torch.cuda.is_available():
@@ -112,13 +126,30 @@ class AstraRuntime:
         self.gelu_mode = 2 if self.fast else 1   # astra_gemm: 2 = bf16-class GELU polynomial
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         self.comm = comm
+        self.sync_params = sync_params
         self.D, self.H, self.L = cfg.hidden, cfg.heads, cfg.layers
         self.dk = cfg.hidden // cfg.heads
         if self.dk not in (4, 8, 16, 32, 64, 128):
             raise ShapeError(f"head_dim {self.dk} unsupported")
         self.T, self.N = plan.tokens, plan.devices
-        self.G, self.K = cfg.groups, cfg.codebook_size
+        # K and G come from the codebooks actually attached (the reference's quantize reads
+        # codebook.size / codebook.groups, vq.py:207-222 — e.g. exact_codebooks_from_reference
+        # builds K = T tables, model.py:405-432); the config's values only size an
+        # unquantized run.
+        books = [b.codebook for b in params.blocks]
+        if any(b is not None for b in books):
+            if any(b is None for b in books):
+                raise LifecycleError("codebooks must be initialized for all layers or none")
+            sizes = {(b.size, b.groups, b.group_dim) for b in books}
+            if len(sizes) != 1:
+                raise ShapeError(f"all layers must share one codebook shape, got {sorted(sizes)}")
+            self.K, self.G, gd = sizes.pop()
+            if self.G * gd != cfg.hidden:
+                raise ShapeError(f"codebook width {self.G * gd} != hidden {cfg.hidden}")
+        else:
+            self.G, self.K = cfg.groups, cfg.codebook_size
         self.bits = index_bits(self.K)
+        _check_fp32(params)
         self.encode_at_one_device = encode_at_one_device
         self.require_codebooks = require_codebooks or plan.devices > 1
         self.capture_inputs = None   # setup hook: per-layer block inputs (codebook fitting)
@@ -165,9 +196,19 @@ class AstraRuntime:
         self.payload_bits = [self.B * s * self.G * self.bits for s in self.sizes]
 
     # ------------------------------------------------------------------ params
+    def _to_dev(self, a) -> torch.Tensor:
+        """Host fp32 array -> HBM.  Under torch.distributed every parameter is then broadcast
+        from rank 0, so all ranks run bit-identical weights and codebooks whatever each
+        process loaded (the reference's devices share one replicated model, cluster.py:259-265)."""
+        arr = np.asarray(a.data if hasattr(a, "data") else a, np.float32)
+        t = torch.from_numpy(np.array(arr, dtype=np.float32, copy=True)).to(self.device)
+        if self.comm is not None and self.sync_params:
+            self.comm.broadcast(t, src=0)
+        return t
+
     def _wt(self, w_in_out: np.ndarray):
         """Reference weight [D_in, D_out] -> B operand [D_out, D_in] (hi[, lo])."""
-        t = torch.from_numpy(np.ascontiguousarray(np.asarray(w_in_out, np.float32).T)).to(self.device)
+        t = self._to_dev(w_in_out).t().contiguous()
         if self.fast:
             return t.to(BF16).contiguous(), None
         hi, lo = kernels.split_bf16(t)
@@ -175,7 +216,7 @@ class AstraRuntime:
 
     def _upload(self, params):
         dev = self.device
-        f32 = lambda a: torch.from_numpy(np.ascontiguousarray(np.asarray(a.data if hasattr(a, "data") else a, np.float32))).to(dev)  # noqa: E501,E731
+        f32 = self._to_dev
         self.layers = []
         for i, bp in enumerate(params.blocks):
             wqkv = np.concatenate([bp.wq.data, bp.wk.data, bp.wv.data], axis=1)
@@ -190,7 +231,7 @@ class AstraRuntime:
                 lay["cb"] = None
             else:
                 tables = np.stack([np.asarray(c, np.float32) for c in bp.codebook.centroids])
-                lay["cb"] = DeviceCodebook(torch.from_numpy(tables).to(dev), layer_id=i)
+                lay["cb"] = DeviceCodebook(f32(tables), layer_id=i)
             self.layers.append(lay)
         self.pos = f32(params.pos)
         self.cls = f32(params.cls).reshape(-1) if params.cls is not None else None
@@ -200,6 +241,7 @@ class AstraRuntime:
         self.classes = params.head.data.shape[1]
         if self.has_remote and self.G == 1:
             self._build_kv_tables()
+        del dev
 
     def _kv_rows(self, lay, x_f32: torch.Tensor, out: torch.Tensor, ln_hi, ln_lo):
         """K|V projection of fp32 rows: LN1 -> [Wk;Wv] GEMM (same kernels as the local path)."""
@@ -256,6 +298,9 @@ class AstraRuntime:
             self.xs_hi = self.xs_lo = self.xnorm = None
             ws = cb0.workspace_bytes(max(self.n_content, 1)) if cb0 else 1
         self.vq_ws = e(max(ws, 1), dt=torch.uint8)
+        # sticky device-side error flags: [0] a received code >= K (unpack / packed key map),
+        # [1] a decode index out of range; read once per forward by check_errors()
+        self.err_flags = torch.zeros(2, dtype=torch.int32, device=dev)
         self.vq_stats = torch.zeros(4, dtype=torch.int32, device=dev)
         self.collect_vq_stats = False   # exactness counters (re-rank rate); off on the hot path
         if self.comm is not None:
@@ -263,7 +308,7 @@ class AstraRuntime:
             self.wmax = max(wmax, 1)
             self.words_local = torch.zeros(self.wmax, dtype=torch.int32, device=dev)
             self.words_all = torch.zeros(self.N * self.wmax, dtype=torch.int32, device=dev)
-            self.unpack_err = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.unpack_err = self.err_flags[0:1]
             self.gofs_dev = torch.tensor(np.asarray(self.gofs, dtype=np.int32), device=dev)
         if self.has_remote and self.G > 1:
             n = self.n_content_all
@@ -271,7 +316,7 @@ class AstraRuntime:
             self.hat_hi = e(n, D, dt=BF16)
             self.hat_lo = None if self.fast else e(n, D, dt=BF16)
             self.kvhat = e(n, 2 * D, dt=BF16 if self.fast else torch.float32)
-            self.dec_err = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.dec_err = self.err_flags[1:2]
         n_rep_local = 0 if self.rep_rows is None else self.rep_rows.numel()
         if self.mode == "generate":
             self._alloc_decode()
@@ -610,6 +655,7 @@ class AstraRuntime:
             host.copy_(self.logits, non_blocking=True)
             main.synchronize()   # the batch's result is on the host
             results.append(host)
+        self.check_errors()
         return results
 
     # ------------------------------------------------------------------ host API
@@ -620,6 +666,16 @@ class AstraRuntime:
         if xs.shape != (self.B, self.T, self.D):
             raise ShapeError(f"expected inputs [{self.B}, {self.T}, {self.D}], got {tuple(xs.shape)}")
         self.x_in.view(self.B, self.T, self.D).copy_(xs, non_blocking=True)
+
+    def check_errors(self) -> None:
+        """Raise IndexCorruptionError if any received / decoded VQ code of the forwards since
+        the last check was outside [0, K) — the reference's dequantize check (vq.py:229-231).
+        One 8-byte device->host read; the flags are cleared after a raise."""
+        f = self.err_flags.cpu().numpy()
+        if f.any():
+            self.err_flags.zero_()
+            where = "in the exchanged payload" if f[0] else "at decode"
+            raise IndexCorruptionError(f"VQ index outside [0, {self.K}) {where}")
 
     def record_ledger(self, ledger):
         if ledger is None or self.N <= 1:
@@ -707,13 +763,27 @@ class AstraRuntime:
                 self._decode_step(out, steps)
         if self.comm is not None:
             self.comm.broadcast(out, src=self.dec_dev)
-        return out[:, :steps].cpu().numpy()
+        res = out[:, :steps].cpu().numpy()
+        self.check_errors()
+        return res
 
     def classify_numpy(self, xs: np.ndarray, ledger=None) -> np.ndarray:
         self.stage_input(xs)
         out = self.run().cpu().numpy().copy()
+        self.check_errors()
         self.record_ledger(ledger)
         return out
 
     def indices_after_layer(self):
         return self.idx_all
+
+    def codes_by_image(self, idx: torch.Tensor) -> np.ndarray:
+        """Codes of every device in global-content order (e, b, r) -> [B, T, G] in global token
+        order per image (what the reference's per-device quantize calls produce, in device order,
+        cluster.py:272-275)."""
+        a = idx.reshape(-1, self.G).cpu().numpy()
+        out = np.empty((self.B, self.T, self.G), a.dtype)
+        for e in range(self.N):
+            blk = a[int(self.gofs[e]):int(self.gofs[e + 1])].reshape(self.B, self.sizes[e], self.G)
+            out[:, self.starts[e]:self.starts[e] + self.sizes[e]] = blk
+        return out

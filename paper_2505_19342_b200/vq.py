@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import zlib
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -157,7 +158,11 @@ class Codebook:
     def on_device(self, device: torch.device | None = None) -> DeviceCodebook:
         """HBM copy (cached per device; codebooks are read-only at inference)."""
         device = device or _device()
-        key = (str(device), tuple(id(c) for c in self.centroids))
+        # identity AND content: ema_update swaps the tables, a caller may edit them in place
+        crc = 0
+        for c in self.centroids:
+            crc = zlib.crc32(np.ascontiguousarray(c).view(np.uint8), crc)
+        key = (str(device), tuple(id(c) for c in self.centroids), crc)
         dc = self._dev.get(key)
         if dc is None:
             tables = np.stack([np.asarray(c, dtype=np.float32) for c in self.centroids])
@@ -185,15 +190,53 @@ class QuantizedTokens:
         return self.token_count * self.bits_per_token
 
 
+def _nearest_f64(x: torch.Tensor, c: torch.Tensor, rows: int = 4096) -> torch.Tensor:
+    """fp64 nearest centroid on the GPU for fp64 models (vq.py:126-131): the reference's
+    expression ``(|p|^2 - 2 p.c) + |c|^2`` in fp64 via cuBLAS DGEMM, argmin with the first
+    index on ties (torch.argmin's contract, like np.argmin)."""
+    cc = (c * c).sum(1)
+    out = torch.empty(x.shape[0], dtype=torch.int64, device=x.device)
+    for r0 in range(0, x.shape[0], rows):
+        p = x[r0:r0 + rows]
+        d2 = (p * p).sum(1, keepdim=True) - 2.0 * (p @ c.T) + cc[None, :]
+        out[r0:r0 + rows] = d2.argmin(1)
+    return out
+
+
+def _quantize_f64(codebook: Codebook, xa, is_torch: bool):
+    dev = xa.device if is_torch and xa.is_cuda else _device()
+    xt = (xa if is_torch else torch.from_numpy(np.ascontiguousarray(xa))).to(dev, torch.float64)
+    gd = codebook.group_dim
+    idx = torch.empty(xt.shape[0], codebook.groups, dtype=torch.int32, device=dev)
+    tables = []
+    for g in range(codebook.groups):
+        c = np.asarray(codebook.centroids[g])
+        ct = torch.from_numpy(np.ascontiguousarray(c, dtype=np.float64)).to(dev)
+        tables.append(torch.from_numpy(np.ascontiguousarray(c)).to(dev))
+        idx[:, g] = _nearest_f64(xt[:, g * gd:(g + 1) * gd].contiguous(), ct).to(torch.int32)
+    # x_hat in the centroids' dtype, groups concatenated in order (vq.py:225-233)
+    xhat = torch.cat([tables[g][idx[:, g].long()] for g in range(codebook.groups)], dim=1)
+    q = QuantizedTokens(codebook.layer_id, xt.shape[0], idx if is_torch else idx.cpu().numpy(),
+                        codebook.bits_per_token)
+    return q, (xhat if is_torch else xhat.cpu().numpy())
+
+
 def quantize(codebook: Codebook, x):
     """Encode tokens to per-group nearest-centroid indices (vq.py:207-222).
 
     Returns (QuantizedTokens, x_hat); x_hat equals dequantize(codebook, indices)
-    bitwise.  Accepts NumPy (returns NumPy) or a CUDA tensor (returns tensors)."""
+    bitwise.  Accepts NumPy (returns NumPy) or a CUDA tensor (returns tensors).
+    fp32 inputs and centroids take the tcgen05 encode (indices bit-identical to the fp64
+    reference); fp64 inputs or centroids take an fp64 GPU search so the reference's fp64
+    semantics are kept, and x_hat comes back in the centroids' dtype."""
     is_torch = isinstance(x, torch.Tensor)
     xa = x if is_torch else np.asarray(x)
     if xa.ndim != 2 or xa.shape[1] != codebook.dim:
         raise ShapeError(f"quantize expects [T, {codebook.dim}], got {tuple(xa.shape)}")
+    c_dtype = np.asarray(codebook.centroids[0]).dtype
+    x_f64 = (xa.dtype == torch.float64) if is_torch else (xa.dtype == np.float64)
+    if x_f64 or c_dtype == np.float64:
+        return _quantize_f64(codebook, xa, is_torch)
     dc = codebook.on_device()
     xt = (xa if is_torch else torch.from_numpy(np.ascontiguousarray(xa, dtype=np.float32)))
     xt = xt.to(dc.centroids.device, torch.float32).contiguous()
@@ -210,6 +253,16 @@ def dequantize(codebook: Codebook, q: QuantizedTokens):
     idx = q.indices
     if idx.shape[1] != codebook.groups:
         raise ShapeError("index width does not match the codebook's groups")
+    if np.asarray(codebook.centroids[0]).dtype != np.float32:
+        # non-fp32 tables (fp64 models): gather in their own dtype, same range check
+        it = idx if isinstance(idx, torch.Tensor) else torch.from_numpy(np.asarray(idx))
+        if it.numel() and (int(it.min()) < 0 or int(it.max()) >= codebook.size):
+            raise IndexCorruptionError(f"index outside [0, {codebook.size}) in layer {q.layer_id}")
+        dev = it.device if it.is_cuda else _device()
+        it = it.to(dev).long()
+        out = torch.cat([torch.from_numpy(np.ascontiguousarray(codebook.centroids[g])).to(dev)[it[:, g]]
+                         for g in range(codebook.groups)], dim=1)
+        return out if isinstance(idx, torch.Tensor) else out.cpu().numpy()
     if isinstance(idx, torch.Tensor):
         return codebook.on_device(idx.device).decode(idx)
     idx = np.asarray(idx)

@@ -1,0 +1,131 @@
+"""Runtime contract: error behaviour, cache invalidation, dtype handling, deterministic
+codebook fitting — the places where the drop-in must behave like the reference beyond
+"same numbers on the happy path"."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import astra_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _small(k=12, layers=1, hidden=64, heads=2, seed=0):
+    from paper_2505_19342_b200 import model, vq
+    cfg = model.ModelConfig(layers=layers, hidden=hidden, heads=heads, vocab_or_classes=5,
+                            max_tokens=33, causal=False, codebook_size=k)
+    p = model.init_params(cfg, seed=seed)
+    rng = np.random.default_rng(seed)
+    for i, b in enumerate(p.blocks):
+        b.codebook = vq.Codebook(layer_id=i, groups=1,
+                                 centroids=[rng.normal(size=(k, hidden)).astype(np.float32) * 0.3])
+    x = rng.normal(size=(32, hidden)).astype(np.float32)
+    return p, x
+
+
+def test_corrupt_exchanged_code_raises(cuda):
+    """A payload code >= K (K=12: 4-bit codes 12..15 are invalid) must raise
+    IndexCorruptionError like the reference's dequantize (vq.py:229-231), not alias row 0."""
+    from paper_2505_19342_b200.cluster import partition_tokens
+    from paper_2505_19342_b200.errors import IndexCorruptionError
+    from paper_2505_19342_b200.runtime import AstraRuntime, LoopbackExchange
+
+    class Corrupting(LoopbackExchange):
+        def all_gather(self, out, inp):
+            super().all_gather(out, inp)
+            out.view(self.world, -1)[1, 0] = -1       # rank 1's first codes -> all ones
+
+    p, x = _small()
+    plan = partition_tokens(32, 2)
+    for precision in ("parity", "fast"):
+        rt = AstraRuntime(p, plan, batch=1, precision=precision, comm=Corrupting(0, 2))
+        with pytest.raises(IndexCorruptionError):
+            rt.classify_numpy(x[None])
+        # flags are cleared after the raise; a clean exchange works again
+        rt.comm = LoopbackExchange(0, 2)
+        rt.classify_numpy(x[None])
+
+
+def test_run_inference_sees_parameter_and_codebook_changes(cuda):
+    """The runtime cache must not serve stale weights or codebooks (cluster.py:224 recomputes
+    from params on every call)."""
+    from paper_2505_19342_b200 import cluster, vq
+    p, x = _small(k=16)
+    plan = cluster.partition_tokens(32, 2)
+    a = cluster.run_inference(p, plan, x, "classify").output
+    assert np.array_equal(cluster.run_inference(p, plan, x, "classify").output, a)
+    p.assign("head", np.asarray(p.head.data) * 2.0)                 # new tensor object
+    b = cluster.run_inference(p, plan, x, "classify").output
+    np.testing.assert_allclose(b, 2.0 * a, rtol=1e-5, atol=1e-7)
+    cb = p.blocks[0].codebook
+    cb.centroids[0][:] = cb.centroids[0][::-1].copy()               # in-place edit
+    c = cluster.run_inference(p, plan, x, "classify").output
+    from paper_2505_19342_b200.runtime import AstraRuntime
+    want = AstraRuntime(p, plan, batch=1).classify_numpy(x[None])
+    np.testing.assert_array_equal(c, want)
+    p.blocks[0].codebook = vq.Codebook(layer_id=0, groups=1, centroids=[cb.centroids[0] + 1.0])
+    d = cluster.run_inference(p, plan, x, "classify").output
+    assert not np.array_equal(d, c)
+
+
+def test_codebook_size_taken_from_attached_codebooks(cuda):
+    """K differs from config.codebook_size (exact_codebooks_from_reference builds K = T)."""
+    from paper_2505_19342_b200 import cluster
+    from paper_2505_19342_b200 import model
+    p, x = _small(k=37)
+    cfg = model.ModelConfig(layers=1, hidden=64, heads=2, vocab_or_classes=5, max_tokens=33,
+                            causal=False, codebook_size=8)
+    p.config = cfg
+    plan = cluster.partition_tokens(32, 4)
+    res = cluster.run_inference(p, plan, x, "classify")
+    op = O.init_params(O.Config(layers=1, hidden=64, heads=2, vocab_or_classes=5, max_tokens=33,
+                                causal=False, codebook_size=37, groups=1), seed=0)
+    op.codebooks = [[np.asarray(b.codebook.centroids[0])] for b in p.blocks]
+    ref = O.run_inference(op, O.partition_tokens(32, 4), x)
+    assert np.abs(res.output - ref.output).max() <= 1e-4
+    assert res.ledger.total_bits_sent() == 32 * 6          # ceil(log2 37) = 6 bits/token
+
+
+def test_quantize_fp64_keeps_reference_semantics(cuda):
+    from paper_2505_19342_b200 import vq
+    rng = np.random.default_rng(3)
+    cents = [rng.normal(size=(50, 16))]                      # fp64 tables
+    cb = vq.Codebook(layer_id=0, groups=1, centroids=cents)
+    x = rng.normal(size=(40, 16))
+    q, xh = vq.quantize(cb, x)
+    np.testing.assert_array_equal(q.indices[:, 0], O.nearest(x, cents[0]))
+    assert xh.dtype == np.float64
+    np.testing.assert_array_equal(xh, cents[0][q.indices[:, 0]])
+    np.testing.assert_array_equal(vq.dequantize(cb, q), xh)
+
+
+def test_argmax_nan_and_all_neg_inf_match_numpy(cuda):
+    from paper_2505_19342_b200 import _native
+    rows = np.array([[1.0, np.nan, 3.0, np.nan], [-np.inf] * 4, [2.0, 5.0, 5.0, 1.0]], np.float32)
+    lt = torch.from_numpy(rows).cuda()
+    out = torch.zeros(3, dtype=torch.int32, device="cuda")
+    _native.call("astra_argmax_rows", lt.data_ptr(), 3, 4, 4, out.data_ptr(), 1, None, 0, None,
+                 torch.cuda.current_stream().cuda_stream)
+    np.testing.assert_array_equal(out.cpu().numpy(), np.argmax(rows, axis=1))
+
+
+def test_gpu_kmeans_equals_reference_lloyd(cuda):
+    """Deterministic GPU k-means (vq.py:134-204): same centroids, counts and sums as the oracle's
+    restatement (pinned to the reference's codebook SHA) on identical samples, incl. a case that
+    forces empty-cluster reseeding."""
+    from paper_2505_19342_b200 import codebooks
+    rng = np.random.default_rng(11)
+    centers = rng.normal(size=(6, 24)) * 4
+    x = (centers[rng.integers(0, 6, 600)] + rng.normal(size=(600, 24)) * 0.2).astype(np.float32)
+    for k, g in ((16, 1), (8, 2), (64, 3)):
+        got = codebooks.kmeans_init(torch.from_numpy(x).cuda(), k, g, iterations=25, seed=4,
+                                    layer_id=2)
+        want = O.kmeans_init(x, k, g, 25, 4, layer_id=2)
+        for gi in range(g):
+            np.testing.assert_array_equal(got.centroids[gi], want[gi])
+    # repeated fits are bitwise identical
+    a = codebooks.kmeans_init(torch.from_numpy(x).cuda(), 16, 1, seed=1)
+    b = codebooks.kmeans_init(torch.from_numpy(x).cuda(), 16, 1, seed=1)
+    np.testing.assert_array_equal(a.centroids[0], b.centroids[0])
+    np.testing.assert_array_equal(a.ema_sums[0], b.ema_sums[0])
