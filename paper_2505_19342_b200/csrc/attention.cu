@@ -1460,6 +1460,291 @@ __global__ void __launch_bounds__(kSThreads, 1)
   }
 }
 
+// ----------------------------------------------------------------------------------------
+// fp32-class (parity mode) attention on tcgen05: the split-bf16 ("bf16x3") scheme of the
+// GEMMs applied to both products of attention (reference op order attention.py:66-72,
+// tensor.py:295-315):
+//   S = Qh Kh^T + Qh Kl^T + Ql Kh^T         (fp32 operands split x = hi + lo on load)
+//   x = S * scale (fp32), p = exp(x - m) (accurate expf), l = sum p in fp32
+//   O = Ph Vh + Ph Vl + Pl Vh               (p = Ph + Pl, split in registers)
+//   out = O / l, written as an fp32 row and/or a bf16 hi/lo split (the next GEMM's operand).
+// One CTA (8 warps) per (segment, head, 128-query tile); keys in 128-key chunks with the
+// online-softmax rescale (ViT-B: 197 keys = 2 chunks), so Q, K and V (hi and lo) take 96 KB
+// of smem and 256 TMEM columns: two CTAs per SM overlap one's softmax with the other's MMAs
+// and gathers.  K/V rows are gathered through key_src (local projection rows or codebook
+// K/V-table rows: the VQ decode fused into the load) from fp32 buffers, split to bf16 hi/lo
+// in registers and stored in the SW128 layout the UMMA descriptors read.  Causal: chunks
+// whose first key lies after the tile's last query are skipped (keys are in global order).
+// TMEM (256 cols): S [0,128) fp32 with Ph packed over it (keys 0-63 -> cols 0-31, keys
+// 64-127 -> cols 64-95), Pl at [128,192), O at [192,256).
+constexpr int kT3Q = 128, kT3KC = 128, kT3Threads = 256;
+constexpr int kT3Tile = 16384;   // 128 rows x 64 bf16, SW128
+constexpr int kT3SmemUsed = 6 * kT3Tile + 256 + 4 * 128 * 4 + 64;
+constexpr int kT3Smem = kT3SmemUsed + 1024;
+
+// 8 fp32 values -> bf16 hi and lo 16-byte chunks at chunk c of row r of two SW128 tiles.
+__device__ __forceinline__ void t3_store_split(const float4& a, const float4& b, uint8_t* hi,
+                                               uint8_t* lo, int r, int c) {
+  const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat162 hh = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    const __nv_bfloat162 ll = __floats2bfloat162_rn(v[2 * i] - __low2float(hh),
+                                                    v[2 * i + 1] - __high2float(hh));
+    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[i] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  const uint32_t off = sw128_offset(r, c);
+  *reinterpret_cast<uint4*>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+__device__ __forceinline__ const float* t3_key_row(const AttnArgs& a, int src, bool v, int hoff) {
+  if (src >= 0)
+    return reinterpret_cast<const float*>(v ? a.v_local : a.k_local) + (size_t)src * a.ld_local + hoff;
+  return reinterpret_cast<const float*>(v ? a.v_remote : a.k_remote) +
+         (size_t)(-(src + 1)) * a.ld_remote + hoff;
+}
+
+__global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                           ~uintptr_t(1023));
+  uint8_t* sQh = sm;
+  uint8_t* sQl = sm + kT3Tile;
+  uint8_t* sKh = sm + 2 * kT3Tile;
+  uint8_t* sKl = sm + 3 * kT3Tile;
+  uint8_t* sVh = sm + 4 * kT3Tile;
+  uint8_t* sVl = sm + 5 * kT3Tile;
+  short* sKpos = reinterpret_cast<short*>(sm + 6 * kT3Tile);
+  float* sRed = reinterpret_cast<float*>(sm + 6 * kT3Tile + 256);   // [max|sum][half][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * kT3Tile + 256 + 2048);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int seg = blockIdx.x, h = blockIdx.y, qt = blockIdx.z;
+  const int* sg = a.segs + seg * 6;
+  const int q0 = sg[0], nq = sg[1], qpos0 = sg[2], ncontent = sg[3], k0 = sg[4], nk = sg[5];
+  if (qt * kT3Q >= nq) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int hoff = h * 64;
+
+  if (warp == 0) tmem_alloc<256>(tslot);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+  }
+  // Q tile: 128 rows x 8 chunks, four (row, chunk) units per thread, loads issued first
+  {
+    float4 qa[4], qb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int u = tid + i * kT3Threads, r = u >> 3, c = u & 7, qr = qt * kT3Q + r;
+      if (qr < nq) {
+        const float* qp = reinterpret_cast<const float*>(a.q) + (size_t)(q0 + qr) * a.ldq + hoff + c * 8;
+        qa[i] = __ldg(reinterpret_cast<const float4*>(qp));
+        qb[i] = __ldg(reinterpret_cast<const float4*>(qp + 4));
+      } else {
+        qa[i] = qb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int u = tid + i * kT3Threads;
+      t3_store_split(qa[i], qb[i], sQh, sQl, u >> 3, u & 7);
+    }
+  }
+
+  const int row = quarter * 32 + lane;             // this thread's query row = TMEM lane
+  const int qi = qt * kT3Q + row;
+  const bool warp_rows = qt * kT3Q + quarter * 32 < nq;
+  const int qpos = qi < ncontent ? qpos0 + qi : 0x7FFE;
+  const int last_q = min(nq, (qt + 1) * kT3Q) - 1;  // causal chunk skipping: tile's last query
+  const int qpos_max = last_q < ncontent ? qpos0 + last_q : 0x7FFE;
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  float m_run = -INFINITY, l_half = 0.f;
+  float o[32];
+#pragma unroll
+  for (int d = 0; d < 32; ++d) o[d] = 0.f;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot, tS = tmem, tPl = tmem + 128, tO = tmem + 192;
+  uint32_t phase = 0;
+
+  const int nchunks = (nk + kT3KC - 1) / kT3KC;
+  for (int c = 0; c < nchunks; ++c) {
+    const int kc = c * kT3KC;
+    if (a.causal && c > 0 && (int)__ldg(a.key_pos + k0 + kc) > qpos_max) break;
+    const int valid = min(kT3KC, nk - kc);
+    const int ncols = (valid + 15) & ~15;
+    // ---- K and V chunk: 2 x 128 rows x 8 chunks = 2048 units, 8 per thread
+    {
+      float4 ka[8], kb[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int u = tid + i * kT3Threads, mv = u >> 10, r = (u >> 3) & 127, cc = u & 7;
+        if (r < valid) {
+          const int src = __ldg(a.key_src + k0 + kc + r);
+          const float* p = t3_key_row(a, src, mv != 0, hoff) + cc * 8;
+          ka[i] = __ldg(reinterpret_cast<const float4*>(p));
+          kb[i] = __ldg(reinterpret_cast<const float4*>(p + 4));
+        } else {
+          ka[i] = kb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int u = tid + i * kT3Threads, mv = u >> 10, r = (u >> 3) & 127, cc = u & 7;
+        t3_store_split(ka[i], kb[i], mv ? sVh : sKh, mv ? sVl : sKl, r, cc);
+      }
+      if (tid < kT3KC)
+        sKpos[tid] = tid < valid ? (a.causal ? (short)__ldg(a.key_pos + k0 + kc + tid) : (short)0)
+                                 : kPosNever;
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      const uint32_t id = idesc_bf16_f32(128, ncols);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        umma_f16(tS, sdesc_kmajor_sw128(smem_u32(sQh) + kk * 32),
+                 sdesc_kmajor_sw128(smem_u32(sKh) + kk * 32), id, kk > 0 ? 1u : 0u);
+        umma_f16(tS, sdesc_kmajor_sw128(smem_u32(sQh) + kk * 32),
+                 sdesc_kmajor_sw128(smem_u32(sKl) + kk * 32), id, 1u);
+        umma_f16(tS, sdesc_kmajor_sw128(smem_u32(sQl) + kk * 32),
+                 sdesc_kmajor_sw128(smem_u32(sKh) + kk * 32), id, 1u);
+      }
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+
+    // ---- pass 1: row max of x = s * scale over this warp's half of the columns
+    float mx = -INFINITY;
+    if (warp_rows) {
+#pragma unroll
+      for (int gg = 0; gg < 2; ++gg) {
+        const int g = half * 2 + gg;
+        if (g * 32 < valid) {
+          uint32_t rr[32];
+          tmem_ld32(tS + lane_off + g * 32, rr);
+          const uint32_t m32 = attn_vis32(sKpos, g * 32, valid, qpos, a.causal);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if ((m32 >> j) & 1u) mx = fmaxf(mx, __uint_as_float(rr[j]) * a.scale);
+        }
+      }
+    }
+    sRed[half * 128 + row] = mx;
+    __syncthreads();
+    const float cmax = fmaxf(sRed[row], sRed[128 + row]);
+    const float mnew = fmaxf(m_run, cmax);
+    const float corr = (m_run == -INFINITY) ? 0.f : expf(m_run - mnew);
+    const float mref = (mnew == -INFINITY) ? 0.f : mnew;
+
+    // ---- pass 2: p = exp(x - m) in fp32, l += p, P = Ph + Pl into TMEM
+    float ls = 0.f;
+    if (warp_rows) {
+#pragma unroll
+      for (int gg = 0; gg < 2; ++gg) {
+        const int g = half * 2 + gg;
+        if (g * 32 < valid) {
+          uint32_t rr[32], ph[16], pl[16];
+          tmem_ld32(tS + lane_off + g * 32, rr);
+          const uint32_t m32 = attn_vis32(sKpos, g * 32, valid, qpos, a.causal);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float p0 = ((m32 >> j) & 1u) ? expf(__uint_as_float(rr[j]) * a.scale - mref) : 0.f;
+            const float p1 =
+                ((m32 >> (j + 1)) & 1u) ? expf(__uint_as_float(rr[j + 1]) * a.scale - mref) : 0.f;
+            ls += p0 + p1;
+            const __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
+            const __nv_bfloat162 ll =
+                __floats2bfloat162_rn(p0 - __low2float(hh), p1 - __high2float(hh));
+            ph[j >> 1] = *reinterpret_cast<const uint32_t*>(&hh);
+            pl[j >> 1] = *reinterpret_cast<const uint32_t*>(&ll);
+          }
+          const int pcol = g < 2 ? g * 16 : 64 + (g - 2) * 16;
+          tmem_st16(tS + lane_off + pcol, ph);
+          tmem_st16(tPl + lane_off + g * 16, pl);
+        }
+      }
+      tmem_st_wait();
+    }
+    l_half = l_half * corr + ls;
+    m_run = mnew;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      const int ksteps = ncols >> 4;
+      const uint32_t id = idesc_bf16_f32_bmn(128, 64);
+      for (int kk = 0; kk < ksteps; ++kk) {
+        const uint32_t acol = kk < 4 ? kk * 8 : 64 + (kk - 4) * 8;
+        const uint64_t dvh = sdesc_mnmajor_sw128(smem_u32(sVh) + kk * 2048, 8192);
+        const uint64_t dvl = sdesc_mnmajor_sw128(smem_u32(sVl) + kk * 2048, 8192);
+        umma_f16_ts(tO, tS + acol, dvh, id, kk > 0 ? 1u : 0u);
+        umma_f16_ts(tO, tS + acol, dvl, id, 1u);
+        umma_f16_ts(tO, tPl + kk * 8, dvh, id, 1u);
+      }
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    if (warp_rows) {
+      uint32_t r0[32];
+      tmem_ld32(tO + lane_off + half * 32, r0);
+      tmem_ld_wait();
+#pragma unroll
+      for (int d = 0; d < 32; ++d) o[d] = fmaf(o[d], corr, __uint_as_float(r0[d]));
+    }
+    tc_fence_before();
+    __syncthreads();   // K/V tiles and TMEM columns are free for the next chunk
+  }
+
+  sRed[256 + half * 128 + row] = l_half;
+  __syncthreads();
+  if (qi < nq) {
+    const float inv = 1.0f / (sRed[256 + row] + sRed[384 + row]);
+    const size_t ob = (size_t)(q0 + qi) * a.ld_out + hoff + half * 32;
+    if (a.out_hi) {
+#pragma unroll
+      for (int d = 0; d < 32; d += 8) {
+        uint32_t wh[4], wl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float v0 = o[d + 2 * u] * inv, v1 = o[d + 2 * u + 1] * inv;
+          const __nv_bfloat162 hh = __floats2bfloat162_rn(v0, v1);
+          const __nv_bfloat162 ll = __floats2bfloat162_rn(v0 - __low2float(hh), v1 - __high2float(hh));
+          wh[u] = *reinterpret_cast<const uint32_t*>(&hh);
+          wl[u] = *reinterpret_cast<const uint32_t*>(&ll);
+        }
+        *reinterpret_cast<uint4*>(a.out_hi + ob + d) = make_uint4(wh[0], wh[1], wh[2], wh[3]);
+        if (a.out_lo)
+          *reinterpret_cast<uint4*>(a.out_lo + ob + d) = make_uint4(wl[0], wl[1], wl[2], wl[3]);
+      }
+    }
+    if (a.out_f32) {
+#pragma unroll
+      for (int d = 0; d < 32; d += 4)
+        *reinterpret_cast<float4*>(a.out_f32 + ob + d) =
+            make_float4(o[d] * inv, o[d + 1] * inv, o[d + 2] * inv, o[d + 3] * inv);
+    }
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
 template <int DH>
 static int launch_attn(const AttnArgs& a, dim3 grid, cudaStream_t st) {
   constexpr int smem = 2 * kAK * (DH + 1) * 4 + kAQ * (kAK + 1) * 4 + kAK * 4;
@@ -1552,6 +1837,28 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
       dim3 tgrid(num_segs, heads, qtiles);
       attention_tc_kernel<<<tgrid, kTcThreads, kTcSmem, st>>>(a);
     }
+    ASTRA_CUDA_CHECK(cudaGetLastError());
+    return ASTRA_OK;
+  }
+  // fp32 inputs (parity mode): the split-bf16 tcgen05 kernel for 64-wide heads
+  const bool aligned32 = (ldq % 4 == 0) && (ld_local % 4 == 0) && (ld_remote % 4 == 0) &&
+                         (ld_out % 8 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k_local) |
+                           reinterpret_cast<uintptr_t>(v_local) |
+                           reinterpret_cast<uintptr_t>(k_remote) |
+                           reinterpret_cast<uintptr_t>(v_remote) |
+                           reinterpret_cast<uintptr_t>(out_f32) |
+                           reinterpret_cast<uintptr_t>(out_hi) |
+                           reinterpret_cast<uintptr_t>(out_lo)) & 15) == 0;
+  if (!in_bf16 && head_dim == 64 && aligned32 && !g_force_simt_attention) {
+    static bool configured3 = false;
+    if (!configured3) {
+      ASTRA_CUDA_CHECK(cudaFuncSetAttribute(attention_tc3_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, kT3Smem));
+      configured3 = true;
+    }
+    dim3 tgrid(num_segs, heads, (max_nq + kT3Q - 1) / kT3Q);
+    attention_tc3_kernel<<<tgrid, kT3Threads, kT3Smem, st>>>(a);
     ASTRA_CUDA_CHECK(cudaGetLastError());
     return ASTRA_OK;
   }

@@ -777,13 +777,14 @@ class AstraRuntime:
     def indices_after_layer(self):
         return self.idx_all
 
-    def codes_by_image(self, idx: torch.Tensor) -> np.ndarray:
-        """Codes of every device in global-content order (e, b, r) -> [B, T, G] in global token
-        order per image (what the reference's per-device quantize calls produce, in device order,
-        cluster.py:272-275)."""
-        a = idx.reshape(-1, self.G).cpu().numpy()
-        out = np.empty((self.B, self.T, self.G), a.dtype)
+    def codes_by_image(self, idx: torch.Tensor, width: int | None = None) -> np.ndarray:
+        """Per-content-row data of every device in global-content order (e, b, r) -> [B, T, width]
+        in global token order per image — for codes (width G, what the reference's per-device
+        quantize calls produce in device order, cluster.py:272-275) or captured rows (width D)."""
+        width = self.G if width is None else width
+        a = idx.reshape(-1, width).cpu().numpy()
+        out = np.empty((self.B, self.T, width), a.dtype)
         for e in range(self.N):
-            blk = a[int(self.gofs[e]):int(self.gofs[e + 1])].reshape(self.B, self.sizes[e], self.G)
+            blk = a[int(self.gofs[e]):int(self.gofs[e + 1])].reshape(self.B, self.sizes[e], width)
             out[:, self.starts[e]:self.starts[e] + self.sizes[e]] = blk
         return out

