@@ -134,16 +134,23 @@ def _parity_block(rt, xs, n, tol):
     rt.forward()
     got = rt.logits.cpu().numpy()
     per_layer = []
+    flipped = np.zeros(len(got), bool)
     for l, t in enumerate(rt.trace):
         codes = rt.codes_by_image(t)[:, :, 0]
-        per_layer.append(float((codes == want_idx[:, l * T:(l + 1) * T]).mean()))
+        eq = codes == want_idx[:, l * T:(l + 1) * T]
+        per_layer.append(float(eq.mean()))
+        flipped |= ~eq.all(axis=1)
     rt.trace = None
     err = float(np.abs(got - want_logits).max())
+    clean = ~flipped
+    err_clean = float(np.abs(got[clean] - want_logits[clean]).max()) if clean.any() else None
     top1 = float((got.argmax(1) == want_logits.argmax(1)).mean())
     return {"reference": f"seqvq run_inference at N={n} on the same weights, codebooks and "
                          f"{len(got)} images (tests/golden/golden_vitb.npz)",
             "top1_agreement": top1, "max_abs_logit_err": err, "logit_tolerance": tol,
             "within_tolerance": err <= tol,
+            "images_with_a_flipped_code": int(flipped.sum()),
+            "max_abs_logit_err_images_without_flips": err_clean,
             "min_layer_index_agreement": min(per_layer) if per_layer else None,
             "indices_bitwise": all(a == 1.0 for a in per_layer),
             "per_layer_index_agreement": [round(a, 6) for a in per_layer]}

@@ -52,7 +52,8 @@ int astra_abi_version(void);
  * passes = 1: A, B are bf16 (fast mode).  passes = 3: A = A_hi + A_lo and
  * B = B_hi + B_lo are split bf16 pairs and the product is computed as
  * hi*hi + hi*lo + lo*hi on tcgen05 (fp32-class parity mode).
- * Requires K % 8 == 0 and 16-byte aligned rows.
+ * K % 8 == 0 with 16-byte aligned rows runs the tcgen05 kernel; any other shape runs a
+ * general SIMT kernel with the same epilogue (fp32 accumulation of hi + lo operands).
  */
 int astra_gemm(const void* a_hi, const void* a_lo, int lda, const void* b_hi, const void* b_lo,
                int ldb, int M, int N, int K, int passes, const float* bias,

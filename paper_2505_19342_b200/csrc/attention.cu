@@ -74,13 +74,14 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
   const int qi = qt * kAQ + r;
   const bool qvalid = qi < nq;
   const int qpos = qi < ncontent ? qpos0 + qi : INT_MAX;
-  const int hoff = h * kDH;
+  const int hd = a.head_dim;   // <= kDH; dims hd..kDH-1 are zero padding
+  const int hoff = h * hd;
 
   float q[kDH];
   {
     const size_t base = (size_t)(q0 + (qvalid ? qi : 0)) * a.ldq + hoff;
 #pragma unroll
-    for (int d = 0; d < kDH; ++d) q[d] = ld_elem<BF16>(a.q, base + d);
+    for (int d = 0; d < kDH; ++d) q[d] = d < hd ? ld_elem<BF16>(a.q, base + d) : 0.f;
   }
   float m = -INFINITY, l = 0.f;
   float acc[kDPT];
@@ -107,8 +108,9 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
         }
 #pragma unroll
         for (int d = 0; d < kDPT; ++d) {
-          sK[kj * kPad + c0 + d] = ld_elem<BF16>(kb, off + d);
-          sV[kj * kPad + c0 + d] = ld_elem<BF16>(vb, off + d);
+          const bool in = c0 + d < hd;
+          sK[kj * kPad + c0 + d] = in ? ld_elem<BF16>(kb, off + d) : 0.f;
+          sV[kj * kPad + c0 + d] = in ? ld_elem<BF16>(vb, off + d) : 0.f;
         }
         if ((tid & 3) == 0) sKpos[kj] = a.key_pos[k0 + j];
       } else {
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
   for (int i = 0; i < kDPT; ++i) {
     const float o = acc[i] * inv;
     const int d = part + 4 * i;
+    if (d >= hd) continue;
     if (a.out_f32) a.out_f32[ob + d] = o;
     if (a.out_hi) {
       __nv_bfloat16 hi, lo;
@@ -1764,6 +1767,17 @@ static int launch_attn(const AttnArgs& a, dim3 grid, cudaStream_t st) {
   return ASTRA_OK;
 }
 
+// SIMT kernel instance for any head width 1..128: the smallest padded width >= head_dim.
+static int launch_attn_any(const AttnArgs& a, dim3 grid, cudaStream_t st) {
+  const int hd = a.head_dim;
+  if (hd <= 4) return launch_attn<4>(a, grid, st);
+  if (hd <= 8) return launch_attn<8>(a, grid, st);
+  if (hd <= 16) return launch_attn<16>(a, grid, st);
+  if (hd <= 32) return launch_attn<32>(a, grid, st);
+  if (hd <= 64) return launch_attn<64>(a, grid, st);
+  return launch_attn<128>(a, grid, st);
+}
+
 }  // namespace astra
 
 using namespace astra;
@@ -1775,9 +1789,8 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
                                int head_dim, int causal, int in_bf16, float scale, float* out_f32,
                                void* out_hi, void* out_lo, int ld_out, int q_rows,
                                int local_rows, int remote_rows, void* stream) {
-  ASTRA_REQUIRE(head_dim == 4 || head_dim == 8 || head_dim == 16 || head_dim == 32 || head_dim == 64 ||
-                    head_dim == 128,
-                ASTRA_ERR_SHAPE, "attention: head_dim %d unsupported", head_dim);
+  ASTRA_REQUIRE(head_dim >= 1 && head_dim <= 128, ASTRA_ERR_SHAPE,
+                "attention: head_dim %d unsupported (1..128)", head_dim);
   ASTRA_REQUIRE(heads >= 1 && num_segs >= 0 && max_nq >= 0, ASTRA_ERR_SHAPE, "attention: bad shape");
   if (num_segs == 0 || max_nq == 0) return ASTRA_OK;
   AttnArgs a{q,       ldq,     k_local, v_local, ld_local, k_remote, v_remote, ld_remote,
@@ -1863,15 +1876,7 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
     return ASTRA_OK;
   }
   dim3 grid(num_segs, heads, (max_nq + kAQ - 1) / kAQ);
-  int rc = ASTRA_OK;
-  switch (head_dim) {
-    case 4: rc = launch_attn<4>(a, grid, st); break;
-    case 8: rc = launch_attn<8>(a, grid, st); break;
-    case 16: rc = launch_attn<16>(a, grid, st); break;
-    case 32: rc = launch_attn<32>(a, grid, st); break;
-    case 64: rc = launch_attn<64>(a, grid, st); break;
-    default: rc = launch_attn<128>(a, grid, st); break;
-  }
+  const int rc = launch_attn_any(a, grid, st);
   if (rc) return rc;
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -1901,8 +1906,7 @@ extern "C" int astra_attention_masked(const float* q, const float* k, const floa
   ASTRA_REQUIRE(heads >= 1 && D % heads == 0, ASTRA_ERR_SHAPE, "width %d not divisible by %d heads",
                 D, heads);
   const int dk = D / heads;
-  ASTRA_REQUIRE(dk == 4 || dk == 8 || dk == 16 || dk == 32 || dk == 64 || dk == 128, ASTRA_ERR_SHAPE,
-                "attention: head_dim %d unsupported", dk);
+  ASTRA_REQUIRE(dk >= 1 && dk <= 128, ASTRA_ERR_SHAPE, "attention: head_dim %d unsupported", dk);
   if (R == 0) return ASTRA_OK;
   std::vector<int32_t> h(6 + 2 * (size_t)C);
   h[0] = 0; h[1] = R; h[2] = 0; h[3] = R; h[4] = 0; h[5] = C;
@@ -1915,14 +1919,5 @@ extern "C" int astra_attention_masked(const float* q, const float* k, const floa
   AttnArgs a{q, D, k, v, D, k, v, D, scratch + 6, scratch + 6 + C, scratch, 1, heads, dk, 0, 0,
              (float)(1.0 / sqrt((double)dk)), out, nullptr, nullptr, D, mask, C};
   dim3 grid(1, heads, (R + kAQ - 1) / kAQ);
-  int rc;
-  switch (dk) {
-    case 4: rc = launch_attn<4>(a, grid, st); break;
-    case 8: rc = launch_attn<8>(a, grid, st); break;
-    case 16: rc = launch_attn<16>(a, grid, st); break;
-    case 32: rc = launch_attn<32>(a, grid, st); break;
-    case 64: rc = launch_attn<64>(a, grid, st); break;
-    default: rc = launch_attn<128>(a, grid, st); break;
-  }
-  return rc;
+  return launch_attn_any(a, grid, st);
 }

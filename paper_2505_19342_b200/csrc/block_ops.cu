@@ -130,7 +130,11 @@ __global__ void embed_stack_kernel(const float* __restrict__ x, const float* __r
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
     const int src = row_src[r];
     float* o = out + (size_t)r * D;
-    if (src >= 0) {
+    if ((D & 3) != 0) {   // general width (small reference configs): scalar path
+      const float* a = src >= 0 ? x + (size_t)src * D : cls;
+      const float* p = pos + (size_t)(src >= 0 ? row_pos[r] : 0) * D;
+      for (int c = lane; c < D; c += 32) o[c] = src >= 0 ? a[c] + p[c] : a[c];
+    } else if (src >= 0) {
       const float* a = x + (size_t)src * D;
       const float* p = pos + (size_t)row_pos[r] * D;
       for (int c = lane * 4; c < D; c += 128) {
@@ -166,8 +170,12 @@ __global__ void gather_rows_kernel(const float* __restrict__ src, int lds,
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
     const float* s = src + (size_t)idx[r] * lds;
     float* o = out + (size_t)r * ldo;
-    for (int c = lane * 4; c < D; c += 128)
-      *reinterpret_cast<float4*>(o + c) = __ldg(reinterpret_cast<const float4*>(s + c));
+    if (((D | lds | ldo) & 3) != 0) {
+      for (int c = lane; c < D; c += 32) o[c] = s[c];
+    } else {
+      for (int c = lane * 4; c < D; c += 128)
+        *reinterpret_cast<float4*>(o + c) = __ldg(reinterpret_cast<const float4*>(s + c));
+    }
   }
 }
 
@@ -373,7 +381,7 @@ extern "C" int astra_layernorm(const float* x, int M, int D, int ldx, const floa
 extern "C" int astra_embed_stack(const float* x, const float* pos, const float* cls,
                                  const int32_t* row_src, const int32_t* row_pos, int rows, int D,
                                  float* out, void* stream) {
-  ASTRA_REQUIRE(D % 4 == 0, ASTRA_ERR_SHAPE, "embed: D must be a multiple of 4");
+  ASTRA_REQUIRE(D >= 1, ASTRA_ERR_SHAPE, "embed: bad width");
   if (rows == 0) return ASTRA_OK;
   embed_stack_kernel<<<grid_rows(rows, 8), 256, 0, as_stream(stream)>>>(x, pos, cls, row_src,
                                                                        row_pos, rows, D, out);
@@ -393,8 +401,7 @@ extern "C" int astra_replica_mean(const float* reps, int N, int B, int D, float*
 
 extern "C" int astra_gather_rows(const float* src, int lds, const int32_t* idx, int rows, int D,
                                  float* out, int ldo, void* stream) {
-  ASTRA_REQUIRE(D % 4 == 0 && lds % 4 == 0 && ldo % 4 == 0, ASTRA_ERR_SHAPE,
-                "gather_rows: widths must be multiples of 4");
+  ASTRA_REQUIRE(D >= 1 && lds >= D && ldo >= D, ASTRA_ERR_SHAPE, "gather_rows: bad widths");
   if (rows == 0) return ASTRA_OK;
   gather_rows_kernel<<<grid_rows(rows, 8), 256, 0, as_stream(stream)>>>(src, lds, idx, rows, D,
                                                                        out, ldo);

