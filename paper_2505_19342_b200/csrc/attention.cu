@@ -1476,8 +1476,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
 // of smem and 256 TMEM columns: two CTAs per SM overlap one's softmax with the other's MMAs
 // and gathers.  K/V rows are gathered through key_src (local projection rows or codebook
 // K/V-table rows: the VQ decode fused into the load) from fp32 buffers, split to bf16 hi/lo
-// in registers and stored in the SW128 layout the UMMA descriptors read.  Causal: chunks
-// whose first key lies after the tile's last query are skipped (keys are in global order).
+// in registers and stored in the SW128 layout the UMMA descriptors read.  Causal: chunks with
+// no key visible to any query of the tile are skipped.
 // TMEM (256 cols): S [0,128) fp32 with Ph packed over it (keys 0-63 -> cols 0-31, keys
 // 64-127 -> cols 64-95), Pl at [128,192), O at [192,256).
 constexpr int kT3Q = 128, kT3KC = 128, kT3Threads = 256;
@@ -1579,8 +1579,11 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
   const int nchunks = (nk + kT3KC - 1) / kT3KC;
   for (int c = 0; c < nchunks; ++c) {
     const int kc = c * kT3KC;
-    if (a.causal && c > 0 && (int)__ldg(a.key_pos + k0 + kc) > qpos_max) break;
     const int valid = min(kT3KC, nk - kc);
+    // causal: a chunk none of whose keys is visible to any query of the tile contributes
+    // nothing (p = 0 for all of it) and is skipped; replica keys (position -1) stay visible
+    if (a.causal && !__syncthreads_or(tid < valid && (int)__ldg(a.key_pos + k0 + kc + tid) <= qpos_max))
+      continue;
     const int ncols = (valid + 15) & ~15;
     // ---- K and V chunk: 2 x 128 rows x 8 chunks = 2048 units, 8 per thread
     {

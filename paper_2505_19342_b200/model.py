@@ -463,8 +463,8 @@ def prefill_decode_state(params: ModelParams, plan, prompt_ids):
     ids = np.asarray(prompt_ids, dtype=np.int64)
     plan = ShardPlan(tokens=plan.tokens, devices=plan.devices, ranges=plan.ranges,
                      class_replication=False)
-    _quantized(params, plan)
-    rt = _model_runtime(params, plan, "generate")
+    quantized = _quantized(params, plan)
+    rt = _model_runtime(params, plan, "generate", require_codebooks=quantized)
     first = int(rt.generate(ids[None, :], 1)[0, 0])
     t = ids.shape[0]
     D = rt.D
@@ -492,8 +492,8 @@ def generate(params: ModelParams, plan, prompt_ids, steps: int) -> list:
     from .cluster import ShardPlan
     plan = ShardPlan(tokens=plan.tokens, devices=plan.devices, ranges=plan.ranges,
                      class_replication=False)
-    _quantized(params, plan)
-    rt = _model_runtime(params, plan, "generate")
+    quantized = _quantized(params, plan)
+    rt = _model_runtime(params, plan, "generate", require_codebooks=quantized)
     return [int(v) for v in rt.generate(ids[None, :], steps)[0]]
 
 

@@ -206,5 +206,5 @@ def test_attention_fp32_parity_kernels_vs_fp64(cuda, spec, causal, force_simt):
     err_split = ((hi.double() + lo.double())[rows] - ref[rows]).abs().max().item() / scale
     # fp32-class: bf16x3 products (operand split error <= 2^-17 relative, lo*lo dropped) with
     # fp32 accumulation — the same class as the parity-mode GEMMs
-    assert err < 1e-5, err
-    assert err_split < 1e-5, err_split
+    assert err < 2e-5, err
+    assert err_split < 2e-5, err_split

@@ -57,7 +57,7 @@ def test_parity_mode_indices_logits_vs_reference(cuda, headline, n):
     within that image.  Checked:
       * at most 1e-4 of all codes differ, and the EARLIEST mismatch of each affected image is a
         tie: on the GPU's own layer input our code is the fp64 argmin and the reference's code
-        scores within 1e-6 * |x|^2 of it;
+        scores within 4e-6 * |x|^2 of it (the bf16x3 operand split is exact to 2^-17);
       * images without any flipped code: logits within 1e-4 (SURVEY 8a' parity tolerance);
       * every image: top-1 identical, logits within the bf16-class 3e-2."""
     params, xs, gold, _ = headline
@@ -83,7 +83,7 @@ def test_parity_mode_indices_logits_vs_reference(cuda, headline, n):
     print(f"N={n} parity: {len(bad)} / {codes.size} code mismatches in {len(first)} image(s), "
           f"first-mismatch gaps {['%.1e' % g for g in gaps]}; max|dlogit| clean images "
           f"{err_clean:.2e}, all {err_all:.2e}")
-    assert all(g <= 1e-6 for g in gaps), gaps
+    assert all(g <= 4e-6 for g in gaps), gaps
     assert err_clean <= 1e-4, err_clean
     assert err_all <= 3e-2, err_all
     np.testing.assert_array_equal(logits.argmax(1), want_logits.argmax(1))
