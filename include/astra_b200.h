@@ -146,6 +146,12 @@ int astra_embed_stack(const float* x, const float* pos, const float* cls, const 
 
 /* aggregate_class_tokens / mean_rows (model.py:268-272, tensor.py:200-208):
  * reps [N, B, D] in device order -> out [B, D], summed in device order then / N. */
+/* LM embed (replaces embed_lm_inputs, model.py:283-288, on the prefill path):
+ * out[r] = emb[ids[row_src[r]]] + pos[row_pos[r]]; ids [B*T] int32 in device memory
+ * (validated by the caller), row_src the stack-row -> b*T + t map. */
+int astra_embed_tokens(const float* emb, const float* pos, const int32_t* ids,
+                       const int32_t* row_src, const int32_t* row_pos, int rows, int D, float* out,
+                       void* stream);
 int astra_replica_mean(const float* reps, int N, int B, int D, float* out, void* stream);
 
 /* out[r, :D] = src[idx[r], :D] (row gather, 16-byte vectors). */

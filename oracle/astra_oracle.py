@@ -372,7 +372,7 @@ def run_inference(params: Params, ranges, x, mode="classify", steps=0, cls_mode=
         owners = list(range(ndev)) if cls_mode == "distributed" else [0]      # model.py:163-169
     x_local = [x0[s:e].copy() for s, e in ranges]
     reps = [params.cls.copy() if d in owners else None for d in range(ndev)]
-    bits = index_bits(cfg.codebook_size)
+    bits = index_bits(params.codebooks[0][0].shape[0])   # the codebook's K (vq.py:74-76)
     res = Result(None, ledger)
     dec_k, dec_v = [], []
     for layer, blk in enumerate(params.blocks):

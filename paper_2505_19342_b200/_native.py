@@ -42,6 +42,7 @@ SIGNATURES: dict[str, list] = {
                         _vp, _c_int, _vp],
     "astra_embed_stack": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _vp],
     "astra_replica_mean": [_vp, _c_int, _c_int, _c_int, _vp, _vp],
+    "astra_embed_tokens": [_vp, _vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _vp],
     "astra_gather_rows": [_vp, _c_int, _vp, _c_int, _c_int, _vp, _c_int, _vp],
     "astra_key_map": [_vp, _c_int, _vp, _vp, _vp],
     "astra_key_map_packed": [_vp, _c_int, _vp, _c_int, _c_int, _c_int, _vp, _c_int, _vp, _vp, _vp],

@@ -20,10 +20,22 @@ from .model import generator
 from .vq import Codebook
 
 
-def capture_block_inputs(params, xs: np.ndarray, device=None) -> list[torch.Tensor]:
-    """Per-layer block inputs (content rows) of a single-device unquantized forward."""
+def capture_block_inputs(params, xs, device=None, mode: str = "classify") -> list[torch.Tensor]:
+    """Per-layer block inputs (content rows) of a single-device unquantized forward over a
+    batch: classify inputs [n, T, D] fp32, or token-id sequences [n, T] for mode="lm"
+    (train.py:160-173 runs classify / lm_logits with an on_layer capture)."""
     from .cluster import partition_tokens
     from .runtime import AstraRuntime
+    if mode == "lm":
+        ids = np.asarray(xs, dtype=np.int64)
+        rt = AstraRuntime(params, partition_tokens(ids.shape[1], 1, class_replication=False),
+                          batch=ids.shape[0], mode="lm", precision="parity", device=device,
+                          encode_at_one_device=False, require_codebooks=False)
+        rt.capture_inputs = []
+        rt.set_ids(ids)
+        rt.forward()
+        torch.cuda.synchronize()
+        return rt.capture_inputs
     xs = np.asarray(xs, dtype=np.float32)
     plan = partition_tokens(xs.shape[1], 1)
     rt = AstraRuntime(params, plan, batch=xs.shape[0], precision="parity", device=device,
@@ -116,12 +128,15 @@ def kmeans_init(x: torch.Tensor, codebook_size: int, groups: int, iterations: in
 
 def fit_codebooks(params, xs: np.ndarray, codebook_size: int | None = None,
                   groups: int | None = None, seed: int = 0, iterations: int = 25,
-                  device=None) -> list[Codebook]:
-    """Fit and attach per-layer codebooks to ``params`` (in place); returns them."""
+                  device=None, mode: str = "classify") -> list[Codebook]:
+    """initialize_codebooks (train.py:176-189) on the GPU: capture, then deterministic
+    per-layer k-means; attaches the books to ``params`` (in place) and returns them."""
     cfg = params.config
     k = codebook_size or cfg.codebook_size
     g_count = groups or cfg.groups
-    caps = capture_block_inputs(params, xs, device=device)
+    for b in params.blocks:
+        b.codebook = None          # capture is the unquantized single-device forward
+    caps = capture_block_inputs(params, xs, device=device, mode=mode)
     books = []
     for layer, x in enumerate(caps):
         cb = kmeans_init(x, k, g_count, iterations=iterations, seed=seed, layer_id=layer)

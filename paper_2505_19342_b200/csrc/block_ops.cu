@@ -333,6 +333,33 @@ __global__ void segment_mean_f64_kernel(const double* __restrict__ pts, int ld,
   if (s1 > s0) mean[(size_t)c * dim + d] = acc / (double)(s1 - s0);
 }
 
+// LM embed (model.py:283-288): out[r] = emb[ids[row_src[r]]] + pos[row_pos[r]].  ids are this
+// step's token ids [B*T] in HBM (staged by one H2D copy), row_src the static stack-row ->
+// (b*T + t) map of the layout, so a new batch needs no host-side index rebuild.
+__global__ void embed_tokens_kernel(const float* __restrict__ emb, const float* __restrict__ pos,
+                                    const int32_t* __restrict__ ids,
+                                    const int32_t* __restrict__ row_src,
+                                    const int32_t* __restrict__ row_pos, int rows, int D,
+                                    float* __restrict__ out) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
+    const float* a = emb + (size_t)ids[row_src[r]] * D;
+    const float* p = pos + (size_t)row_pos[r] * D;
+    float* o = out + (size_t)r * D;
+    if ((D & 3) != 0) {
+      for (int c = lane; c < D; c += 32) o[c] = a[c] + p[c];
+    } else {
+      for (int c = lane * 4; c < D; c += 128) {
+        const float4 va = __ldg(reinterpret_cast<const float4*>(a + c));
+        const float4 vp = __ldg(reinterpret_cast<const float4*>(p + c));
+        *reinterpret_cast<float4*>(o + c) =
+            make_float4(va.x + vp.x, va.y + vp.y, va.z + vp.z, va.w + vp.w);
+      }
+    }
+  }
+}
+
 extern "C" int astra_layernorm_ex(const float* x, int M, int D, int ldx, const float* gain,
                                   const float* bias, float eps, float* out_f32, int ld_f32,
                                   void* out_hi, void* out_lo, int ld_bf, void* xs_hi, void* xs_lo,
@@ -509,6 +536,17 @@ extern "C" int astra_segment_mean_f64(const double* pts, int ld, const int32_t* 
   dim3 grid((dim + 127) / 128, k);
   segment_mean_f64_kernel<<<grid, 128, 0, as_stream(stream)>>>(pts, ld, order, seg, k, dim, mean,
                                                               sums);
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_embed_tokens(const float* emb, const float* pos, const int32_t* ids,
+                                  const int32_t* row_src, const int32_t* row_pos, int rows, int D,
+                                  float* out, void* stream) {
+  ASTRA_REQUIRE(rows >= 0 && D >= 1, ASTRA_ERR_SHAPE, "embed_tokens: bad shape");
+  if (rows == 0) return ASTRA_OK;
+  embed_tokens_kernel<<<grid_rows(rows, 8), 256, 0, as_stream(stream)>>>(emb, pos, ids, row_src,
+                                                                        row_pos, rows, D, out);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }

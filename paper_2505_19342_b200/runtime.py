@@ -275,6 +275,7 @@ class AstraRuntime:
         dev, R, D, B = self.device, self.R, self.D, self.B
         e = lambda *s, dt=torch.float32: torch.empty(*s, dtype=dt, device=dev)  # noqa: E731
         self.x_in = e(B * self.T, D)
+        self.id_slots = [torch.zeros(B * self.T, dtype=torch.int32, device=dev)]
         self.X, self.Hres = e(R, D), e(R, D)
         self.ln_hi = e(R, D, dt=BF16)
         self.ln_lo = None if self.fast else e(R, D, dt=BF16)
@@ -370,6 +371,7 @@ class AstraRuntime:
         self.dec_f_lo = None if self.fast else torch.empty(B, 4 * D, dtype=BF16, device=dev)
         self.dec_logits = torch.empty(B, self.classes, device=dev)
         self.next_tok = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.first_out = torch.zeros(B, dtype=torch.int32, device=dev)
         self.dec_pos = torch.zeros(B, dtype=torch.int32, device=dev)
         self.dec_segs = torch.zeros(B * 6, dtype=torch.int32, device=dev)
         self.dec_key_src = i32([b * self.maxT + j for b in range(B) for j in range(self.maxT)])
@@ -536,7 +538,12 @@ class AstraRuntime:
 
     def _embed(self):
         # classify: x + pos (model.py:275-280); generate: embedding[ids] + pos (model.py:283-288)
-        x_in = self.emb if self.mode in ("generate", "lm") else self.x_slots[self._slot]
+        if self.mode in ("generate", "lm"):
+            _native.call("astra_embed_tokens", self.emb.data_ptr(), self.pos.data_ptr(),
+                         self.id_slots[self._slot].data_ptr(), self.row_src.data_ptr(),
+                         self.row_pos.data_ptr(), self.R, self.D, self.X.data_ptr(), _stream())
+            return
+        x_in = self.x_slots[self._slot]
         pos = self.pos_zero if self.mode == "blocks" else self.pos
         _native.call("astra_embed_stack", x_in.data_ptr(), pos.data_ptr(),
                      _p(self.cls), self.row_src.data_ptr(), self.row_pos.data_ptr(), self.R,
@@ -586,7 +593,17 @@ class AstraRuntime:
         if self.mode == "lm":
             self._lm_tail()
             return self.lm_out
+        if self.mode == "generate" and self.decodes:
+            self._first_token()
+            return self.first_out
         return None
+
+    def _first_token(self):
+        """End of the prefill (cluster.py:299-302): greedy first token of every sequence from
+        the decoding device's last row -> first_out / next_tok."""
+        _native.call("astra_gather_rows", self.X.data_ptr(), self.D, self.last_rows.data_ptr(),
+                     self.B, self.D, self.dec_X.data_ptr(), self.D, _stream())
+        self._head_argmax(self.dec_X, self.first_out, 1, first=True)
 
     def _lm_tail(self):
         """lm_logits (model.py:305-313): final LN and head over every content row (causal
@@ -599,11 +616,16 @@ class AstraRuntime:
         kernels.gemm(self.lm_ln_hi, whi, a_lo=self.lm_ln_lo, b_lo=wlo, out_f32=self.lm_out)
 
     # -------------------------------------------------------------- CUDA graph
+    def _add_slots(self, slots: int):
+        while len(self.x_slots) < slots:
+            self.x_slots.append(torch.empty_like(self.x_in))
+        while len(self.id_slots) < slots:
+            self.id_slots.append(torch.zeros_like(self.id_slots[0]))
+
     def capture(self, warmup: int = 1, slots: int = 1):
         """Record ``forward`` (fixed buffers, fixed launch sequence) into CUDA graphs, one per
         input slot (two slots let the next batch's host->device copy overlap this forward)."""
-        while len(self.x_slots) < slots:
-            self.x_slots.append(torch.empty_like(self.x_in))
+        self._add_slots(slots)
         for _ in range(warmup):
             self.forward()
         torch.cuda.synchronize()
@@ -627,20 +649,17 @@ class AstraRuntime:
             self._slot = 0
         return getattr(self, "logits", None)
 
-    def classify_stream(self, batches, out=None):
-        """Serve a sequence of host batches ([B, T, D] fp32, pinned for async copies).
-
-        Double-buffered: the host->device copy of batch i+1 runs on a copy stream while
-        batch i's forward runs; every batch's logits are copied back and synchronised
-        before the next result is produced.  Returns the list of host logits tensors."""
+    def _serve(self, batches, out, stage, result):
+        """Double-buffered serving loop: the host->device copy of batch i+1 (``stage``) runs on
+        a copy stream while batch i's forward runs; each batch's ``result`` is copied back and
+        synchronised before the next is produced."""
         if len(self.x_slots) < 2:
             try:
                 self.capture(slots=2)
             except RuntimeError:   # e.g. a collective that cannot be graph-captured: eager
                 torch.cuda.synchronize()
                 self.graph, self.graphs = None, []
-                while len(self.x_slots) < 2:
-                    self.x_slots.append(torch.empty_like(self.x_in))
+                self._add_slots(2)
         main = torch.cuda.current_stream()
         copy = getattr(self, "_copy_stream", None) or torch.cuda.Stream(device=self.device)
         self._copy_stream = copy
@@ -648,19 +667,13 @@ class AstraRuntime:
         done = [torch.cuda.Event() for _ in range(2)]
         results = []
         n = len(batches)
-        start, stop = ((0, self.T) if self.comm is None else self.plan.ranges[self.comm.rank])
 
         def h2d(i):
             slot = i % 2
             with torch.cuda.stream(copy):
                 if i >= 2:
                     copy.wait_event(done[slot])
-                xv = self.x_slots[slot].view(self.B, self.T, self.D)
-                src = batches[i]
-                if self.comm is None:
-                    xv.copy_(src, non_blocking=True)
-                else:  # only this rank's token shard crosses PCIe
-                    xv[:, start:stop].copy_(src, non_blocking=True)
+                stage(slot, batches[i])
                 copied[slot].record(copy)
 
         if n:
@@ -672,13 +685,38 @@ class AstraRuntime:
             done[slot].record(main)
             if i + 1 < n:
                 h2d(i + 1)
-            host = out[i] if out is not None else torch.empty(self.logits.shape, dtype=torch.float32,
+            host = out[i] if out is not None else torch.empty(result.shape, dtype=result.dtype,
                                                               pin_memory=True)
-            host.copy_(self.logits, non_blocking=True)
+            host.copy_(result, non_blocking=True)
             main.synchronize()   # the batch's result is on the host
             results.append(host)
         self.check_errors()
         return results
+
+    def classify_stream(self, batches, out=None):
+        """Serve host batches ([B, T, D] fp32, pinned; under torchrun this rank's token shard
+        [B, T_d, D]) -> host logits per batch."""
+        start, stop = ((0, self.T) if self.comm is None else self.plan.ranges[self.comm.rank])
+
+        def stage(slot, src):
+            xv = self.x_slots[slot].view(self.B, self.T, self.D)
+            if self.comm is None:
+                xv.copy_(src, non_blocking=True)
+            else:  # only this rank's token shard crosses PCIe
+                xv[:, start:stop].copy_(src, non_blocking=True)
+
+        return self._serve(batches, out, stage, self.logits)
+
+    def prefill_stream(self, batches, out=None):
+        """Serve host token-id batches ([B, T] int32, pinned) through the SP causal prefill ->
+        the first greedy token of every sequence (host int32 [B]) per batch."""
+        if self.mode != "generate":
+            raise ValueError("runtime was not built for generate mode")
+
+        def stage(slot, src):
+            self.id_slots[slot].view(self.B, self.T).copy_(src, non_blocking=True)
+
+        return self._serve(batches, out, stage, self.first_out)
 
     # ------------------------------------------------------------------ host API
     def stage_input(self, xs):
@@ -757,17 +795,13 @@ class AstraRuntime:
         self._head_argmax(X, out, steps, first=False)
         _native.call("astra_decode_advance", self.dec_pos.data_ptr(), self.dec_segs.data_ptr(), B, s)
 
-    def set_ids(self, ids) -> None:
-        """Token ids [B, T] -> embed map rows (embedding[ids] + pos, model.py:283-288)."""
+    def set_ids(self, ids, slot: int = 0) -> None:
+        """Stage token ids [B, T] (embedding[ids] + pos, model.py:283-288) into HBM."""
         B, T = self.B, self.T
         ids = np.asarray(ids, dtype=np.int64).reshape(B, T)
         if ids.size and (ids.min() < 0 or ids.max() >= self.emb.shape[0]):
             raise ShapeError("gather_rows: id out of range")
-        src = np.empty(self.R, dtype=np.int32)
-        for (v, b), base in self.row_base.items():
-            st, n = self.starts[v], self.sizes[v]
-            src[base:base + n] = ids[b, st:st + n]
-        self.row_src.copy_(torch.from_numpy(src))
+        self.id_slots[slot].copy_(torch.from_numpy(ids.astype(np.int32).reshape(-1)))
 
     def lm_logits(self, ids) -> np.ndarray:
         """[B, T, vocab] next-token logits of every position (mode "lm")."""
@@ -810,12 +844,10 @@ class AstraRuntime:
         T = self.T
         self.set_ids(ids)
         out = torch.zeros(B, max(steps, 1), dtype=torch.int32, device=dev)
-        self.forward()
+        self.run()
         self.record_ledger(ledger)
         if self.decodes and steps > 0:
-            _native.call("astra_gather_rows", self.X.data_ptr(), self.D, self.last_rows.data_ptr(),
-                         B, self.D, self.dec_X.data_ptr(), self.D, _stream())
-            self._head_argmax(self.dec_X, out, steps, first=True)
+            out[:, 0].copy_(self.first_out)
             segs = np.array([[b, 1, T, 1, b * self.maxT, T + 1] for b in range(B)], np.int32)
             self.dec_segs.copy_(torch.from_numpy(segs.reshape(-1)))
             self.dec_pos.fill_(T)
