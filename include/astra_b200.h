@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define ASTRA_ABI_VERSION 1
+#define ASTRA_ABI_VERSION 2
 
 /* status codes; the Python shim maps them to the reference's exception types
  * (seqvq/errors.py:4-33). */
@@ -81,9 +81,11 @@ typedef struct AstraCodebook {
   const float* c_sq;        /* [G, K] ||c||^2 (fp32, epilogue score)          */
   const double* c_sq64;     /* [G, K] ||c||^2 (fp64, exact re-rank)           */
   const float* c_norm_max;  /* [G] max_k ||c_k||                              */
+  const void* c_win;        /* [G, K] float4 {||c||^2, ||c|| (rounded up), 4.8e-7 ||c||^2, 0}:
+                               per-code score error window of the encode epilogue */
 } AstraCodebook;
 
-/* Fill the derived tables of `cb` (c_hi, c_lo, c_sq, c_sq64, c_norm_max are
+/* Fill the derived tables of `cb` (c_hi, c_lo, c_sq, c_sq64, c_norm_max, c_win are
  * caller-allocated device buffers named in cb; cb->centroids is the input). */
 int astra_vq_prepare(const AstraCodebook* cb, void* stream);
 
@@ -207,7 +209,11 @@ int astra_segment_mean_f64(const double* pts, int ld, const int32_t* order, cons
  * segs[S, 6] = {q0, nq, qpos0, ncontent, k0, nk} per (device, image) segment;
  * key_src (see astra_key_map) picks local or remote K/V rows; key_pos is the
  * global token position (-1 = class replica key); visible iff !causal ||
- * key_pos <= query_pos.  head_dim must be 64.  in_bf16 selects bf16 inputs. */
+ * key_pos <= query_pos.  causal = 2 additionally promises prefix keys (key j of every
+ * segment has position j, no replica key), so key chunks past a query tile's last position
+ * are skipped.  head_dim 1..128 (64: tcgen05 kernels; fp32 inputs take the split-bf16
+ * parity kernel).  in_bf16 selects bf16 inputs; out_hi/out_lo receive the bf16 (split) output,
+ * out_f32 the fp32 one. */
 int astra_attention(const void* q, int ldq, const void* k_local, const void* v_local, int ld_local,
                     const void* k_remote, const void* v_remote, int ld_remote,
                     const int32_t* key_src, const int32_t* key_pos, const int32_t* segs,

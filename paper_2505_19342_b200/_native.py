@@ -14,7 +14,7 @@ from pathlib import Path
 from .errors import IndexCorruptionError, MaskError, ShapeError
 
 _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libastra_b200.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _c_int = ctypes.c_int
 _c_ll = ctypes.c_longlong

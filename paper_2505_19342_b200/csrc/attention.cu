@@ -560,6 +560,10 @@ struct PIter {
         cur.ncontent = e.ncontent;
         cur.k0 = e.k0;
         cur.nk = e.nk;
+        if (a.causal == 2) {   // prefix keys (key j at position j): later keys are invisible
+          const int last = min(e.nq, (e.qt + 1) * kTQ) - 1;
+          if (last < e.ncontent) cur.nk = min(e.nk, e.qpos0 + last + 1);
+        }
         cur.h = e.h;
         cur.qt = e.qt;
         cur.kc = 0;

@@ -4,7 +4,7 @@
 // fp64 and takes argmin with ties -> lowest index; vq.quantize (vq.py:207-222)
 // runs it per group; vq.dequantize (vq.py:225-233) gathers centroid rows.
 //
-// Encode on B200 = three kernels:
+// Encode on B200 = three kernels (plus the fp64 re-rank of multi-candidate rows):
 //   1. vq_split      fp32 token rows -> bf16 hi/lo split, one zero-padded [M, 64k] slab per
 //                    group, and ||x_g|| (for the error window).
 //   2. tc_gemm<VqEpilogue>  tcgen05 bf16x3 distance GEMM (scores = ||c||^2 - 2 x.c, the
@@ -19,7 +19,9 @@
 // differs from x.c by at most 3.02 * 2^-16 * sum|x_i c_i| <= 3.02 * 2^-16 ||x|| ||c||
 // (Cauchy-Schwarz) plus fp32 accumulation error; kTau = 2^-14 covers the former with 30%
 // headroom left for the latter (measured |err| ~ 1.3e-6 ||x|| ||c||).  Score error is 2x
-// that plus fp32 rounding of the epilogue arithmetic.
+// that plus fp32 rounding of the epilogue arithmetic — bounded PER CODE with ||c_k|| (see
+// window_a), so a code is a candidate iff its lower bound s_k - D_k reaches the best upper
+// bound min_j (s_j + D_j).
 #include "host_common.h"
 #include "tc_gemm.cuh"
 
@@ -36,10 +38,12 @@ struct VqWorkspace {
   __nv_bfloat16* x_hi;
   __nv_bfloat16* x_lo;
   float* x_norm;      // [G, M]
-  float* rec_best;    // [G, M, nchunk]
+  float* rec_best;    // [G, M, nchunk] U_chunk = min_j (s_j + D_j): an upper bound of the true
+                      // best score among the chunk's codes
+  float* rec_lmin;    // [G, M, nchunk] min_j (s_j - D_j) over the chunk
   int* rec_cnt;       // [G, M, nchunk]
   int* rec_idx;       // [G, M, nchunk, cap]
-  float* rec_score;   // [G, M, nchunk, cap]
+  float* rec_score;   // [G, M, nchunk, cap] lower bounds L_k = s_k - D_k of the candidates
   int* rr_list;       // [G * M][kRREntry] items whose window holds > 1 candidate (fp64 re-rank):
                       // {item, n (-1: scan the records), candidate codes ...}
   int* rr_count;      // [1]
@@ -59,6 +63,7 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
   size_t o_lo = take((size_t)G * M * gdp * 2);
   size_t o_norm = take((size_t)G * M * 4);
   size_t o_best = take((size_t)G * M * nchunk * 4);
+  size_t o_lmin = take((size_t)G * M * nchunk * 4);
   size_t o_cnt = take((size_t)G * M * nchunk * 4);
   size_t o_idx = take((size_t)G * M * nchunk * kVqCap * 4);
   size_t o_sc = take((size_t)G * M * nchunk * kVqCap * 4);
@@ -70,6 +75,7 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
     w->x_lo = reinterpret_cast<__nv_bfloat16*>(b + o_lo);
     w->x_norm = reinterpret_cast<float*>(b + o_norm);
     w->rec_best = reinterpret_cast<float*>(b + o_best);
+    w->rec_lmin = reinterpret_cast<float*>(b + o_lmin);
     w->rec_cnt = reinterpret_cast<int*>(b + o_cnt);
     w->rec_idx = reinterpret_cast<int*>(b + o_idx);
     w->rec_score = reinterpret_cast<float*>(b + o_sc);
@@ -79,10 +85,15 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
   return off;
 }
 
-// Half-width of the score error window for a token of norm xn against codes of norm <= cmax.
-__device__ __forceinline__ float score_delta(float xn, float cmax) {
-  return 2.0f * kTau * xn * cmax + 4.8e-7f * (cmax * cmax + 2.0f * xn * cmax) + 1e-30f;
-}
+// Error bound of the computed score s_k = ||c_k||^2 - 2 x.c_k (bf16x3 dot product, fp32
+// epilogue) for a token of norm <= xn and a code of norm <= n_k:
+//   D_k = 2 tau xn n_k + eps (n_k^2 + 2 xn n_k) = n_k (a + eps n_k) + tiny, a = (2 tau + 2 eps) xn.
+// Per code, not per codebook: the true argmin k* satisfies s_k* - D_k* <= true score of k* <=
+// true score of any j <= s_j + D_j, so every code with L_k = s_k - D_k above
+// U = min_j (s_j + D_j) is excluded — a window of D_best + D_k instead of 4 tau xn max||c||
+// (layer-input codebooks span ||c|| from ~0.2x to 1x of the max, so this is 2-6x tighter).
+constexpr float kEps = 4.8e-7f;
+__device__ __forceinline__ float window_a(float xn) { return (2.0f * kTau + 2.0f * kEps) * xn; }
 
 // ------------------------------------------------------------ prepare
 __global__ void vq_prepare_kernel(AstraCodebook cb) {
@@ -108,6 +119,9 @@ __global__ void vq_prepare_kernel(AstraCodebook cb) {
   if (lane == 0) {
     ((double*)cb.c_sq64)[code] = s64;
     ((float*)cb.c_sq)[code] = (float)s64;
+    // per-code window terms: ||c|| rounded up, and the fp32-epilogue rounding term
+    const float n = (float)sqrt(s64) * (1.0f + 1e-6f);
+    ((float4*)cb.c_win)[code] = make_float4((float)s64, n, kEps * n * n, 0.f);
   }
 }
 
@@ -160,8 +174,7 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
 template <int BN>
 struct VqEpilogue {
   int M, K, nchunk;         // nchunk = records per (g, row): kEpiParts per BN-code tile
-  const float* c_sq;        // [G, K]
-  const float* c_norm_max;  // [G]
+  const float4* c_win;      // [G, K] {||c||^2, ||c||, eps ||c||^2, 0}
   VqWorkspace w;
 
   __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
@@ -170,44 +183,23 @@ struct VqEpilogue {
     const bool ok = row < M;
     const int g = tc.batch;
     const int col_base = tc.n_blk * BN;
-    const float* csq = c_sq + (size_t)g * K;
-    float best = INFINITY;
-    // ||c||^2 of the 32 columns of a chunk: one coalesced load per warp, broadcast from smem
-    // (columns >= K get +inf, so they never win and never enter the window)
-    float* scs = reinterpret_cast<float*>(stage);
+    const float4* cw = c_win + (size_t)g * K;
+    // window terms of the 32 columns of a chunk: one coalesced 16-byte load per lane,
+    // broadcast from smem (columns >= K get ||c||^2 = +inf: never a candidate, U unaffected)
+    float4* scs = reinterpret_cast<float4*>(stage);
     const int lane = threadIdx.x & 31;
     // the re-rank list count for the finalize kernel that follows (stream order): reset by
     // one thread here instead of a memset node in front of this GEMM
     if (tc.m_blk == 0 && tc.n_blk == 0 && g == 0 && row_in_tile == 0 && cb == 0) *w.rr_count = 0;
-    float bst[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
-#pragma unroll 1
-    for (int c0 = cb; c0 < ce; c0 += 32) {
-      const int col0 = col_base + c0;
-      const float cl = (col0 + lane < K) ? __ldg(csq + col0 + lane) : INFINITY;
-      uint32_t r[32];
-      tmem_ld32(taddr + c0, r);
-      tmem_ld_wait();
-      scs[lane] = cl;
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        const float4 q = *reinterpret_cast<const float4*>(scs + j);
-        bst[0] = fminf(bst[0], fmaf(-2.0f, __uint_as_float(r[j]), q.x));
-        bst[1] = fminf(bst[1], fmaf(-2.0f, __uint_as_float(r[j + 1]), q.y));
-        bst[2] = fminf(bst[2], fmaf(-2.0f, __uint_as_float(r[j + 2]), q.z));
-        bst[3] = fminf(bst[3], fmaf(-2.0f, __uint_as_float(r[j + 3]), q.w));
-      }
-      __syncwarp();
-    }
-    best = fminf(fminf(bst[0], bst[1]), fminf(bst[2], bst[3]));
     const float xn = ok ? w.x_norm[(size_t)g * M + row] : 0.f;
-    const float thr = best + 2.0f * score_delta(xn, __ldg(c_norm_max + g));
-    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk * kEpiParts + part;
-    int cnt = 0;
+    const float a = window_a(xn);
+    // pass 1: U = min_j (s_j + D_j)
+    float ub[2] = {INFINITY, INFINITY};
 #pragma unroll 1
     for (int c0 = cb; c0 < ce; c0 += 32) {
       const int col0 = col_base + c0;
-      const float cl = (col0 + lane < K) ? __ldg(csq + col0 + lane) : INFINITY;
+      const float4 cl = (col0 + lane < K) ? __ldg(cw + col0 + lane)
+                                          : make_float4(INFINITY, 0.f, 0.f, 0.f);
       uint32_t r[32];
       tmem_ld32(taddr + c0, r);
       tmem_ld_wait();
@@ -215,22 +207,46 @@ struct VqEpilogue {
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const int col = col0 + j;
-        if (col < K) {
-          const float s = fmaf(-2.0f, __uint_as_float(r[j]), scs[j]);
-          if (s <= thr) {
-            if (ok && cnt < kVqCap) {
-              w.rec_idx[rec * kVqCap + cnt] = col;
-              w.rec_score[rec * kVqCap + cnt] = s;
-            }
-            ++cnt;
+        const float4 q = scs[j];
+        const float sc = fmaf(-2.0f, __uint_as_float(r[j]), q.x);
+        ub[j & 1] = fminf(ub[j & 1], sc + fmaf(a, q.y, q.z));
+      }
+      __syncwarp();
+    }
+    const float U = fminf(ub[0], ub[1]) + 1e-30f;
+    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk * kEpiParts + part;
+    // pass 2: candidates L_k = s_k - D_k <= U (the chunk's own U; the finalize applies the
+    // global one), and the chunk's min L
+    int cnt = 0;
+    float lmin = INFINITY;
+#pragma unroll 1
+    for (int c0 = cb; c0 < ce; c0 += 32) {
+      const int col0 = col_base + c0;
+      const float4 cl = (col0 + lane < K) ? __ldg(cw + col0 + lane)
+                                          : make_float4(INFINITY, 0.f, 0.f, 0.f);
+      uint32_t r[32];
+      tmem_ld32(taddr + c0, r);
+      tmem_ld_wait();
+      scs[lane] = cl;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float4 q = scs[j];
+        const float lo = fmaf(-2.0f, __uint_as_float(r[j]), q.x) - fmaf(a, q.y, q.z);
+        lmin = fminf(lmin, lo);
+        if (lo <= U && col0 + j < K) {
+          if (ok && cnt < kVqCap) {
+            w.rec_idx[rec * kVqCap + cnt] = col0 + j;
+            w.rec_score[rec * kVqCap + cnt] = lo;
           }
+          ++cnt;
         }
       }
       __syncwarp();
     }
     if (ok) {
-      w.rec_best[rec] = best;
+      w.rec_best[rec] = U;
+      w.rec_lmin[rec] = lmin;
       w.rec_cnt[rec] = cnt;
     }
   }
@@ -263,27 +279,27 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
   const int warps = blockDim.x >> 5;
   const int item = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  const int G = cb.groups, K = cb.size, gd = cb.group_dim;
+  const int G = cb.groups;
   if (item >= G * M) return;
   const int g = item / M, row = item % M;
-  // records / norms are indexed by token (gathered split) or by source row (pre-split stack)
+  // records are indexed by token (gathered split) or by source row (pre-split stack)
   const int rr = rec_by_row ? rows[row] : row;
   const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
   // one round of independent loads: lane c holds chunk record c (nchunk <= 32 for K <= 2048;
   // larger codebooks loop)
-  const float xn = w.x_norm[(size_t)g * Mrec + rr];
-  const float cmax = cb.c_norm_max[g];
+  // U = min over chunks of U_chunk bounds the true best score from above; a chunk matters if
+  // its min lower bound reaches U, a candidate if its own lower bound L_k does
   float best = INFINITY;
   int n = 0, only = 0x7FFFFFFF;
   int overflow = 0;
-  float thr = 0.f;
   uint32_t live = 0;
   int ix[kVqCap];
   if (nchunk <= 32) {
-    float rb = INFINITY, sc[kVqCap];
+    float rb = INFINITY, rl = INFINITY, sc[kVqCap];
     int rc = 0;
     if (lane < nchunk) {
       rb = w.rec_best[rec0 + lane];
+      rl = w.rec_lmin[rec0 + lane];
       rc = w.rec_cnt[rec0 + lane];
 #pragma unroll
       for (int i = 0; i < kVqCap; ++i) {
@@ -293,12 +309,11 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
     }
     best = rb;
     for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
-    thr = best + 2.0f * score_delta(xn, cmax);
-    if (lane < nchunk && rb <= thr) {
+    if (lane < nchunk && rl <= best) {
       if (rc > kVqCap) overflow = 1;
 #pragma unroll
       for (int i = 0; i < kVqCap; ++i)
-        if (i < rc && sc[i] <= thr) {
+        if (i < rc && sc[i] <= best) {
           ++n;
           only = min(only, ix[i]);
           live |= 1u << i;
@@ -308,14 +323,13 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
     overflow = 1;   // wide codebooks: the re-rank kernel scans the records
     for (int c = lane; c < nchunk; c += 32) best = fminf(best, w.rec_best[rec0 + c]);
     for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
-    thr = best + 2.0f * score_delta(xn, cmax);
     for (int c = lane; c < nchunk; c += 32) {
-      if (w.rec_best[rec0 + c] > thr) continue;
+      if (w.rec_lmin[rec0 + c] > best) continue;
       const int cnt = w.rec_cnt[rec0 + c];
       if (cnt > kVqCap) overflow = 1;
       const int m = cnt < kVqCap ? cnt : kVqCap;
       for (int i = 0; i < m; ++i)
-        if (w.rec_score[(rec0 + c) * kVqCap + i] <= thr) {
+        if (w.rec_score[(rec0 + c) * kVqCap + i] <= best) {
           ++n;
           only = min(only, w.rec_idx[(rec0 + c) * kVqCap + i]);
         }
@@ -438,11 +452,9 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
     }
     const int rr = rec_by_row ? rows[row] : row;
     const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
-    const float xn = w.x_norm[(size_t)g * Mrec + rr];
-    float best = INFINITY;
-    for (int c = lane; c < nchunk; c += 32) best = fminf(best, w.rec_best[rec0 + c]);
-    for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
-    const float thr = best + 2.0f * score_delta(xn, cb.c_norm_max[g]);
+    float thr = INFINITY;   // U: min over the chunks' upper bounds
+    for (int c = lane; c < nchunk; c += 32) thr = fminf(thr, w.rec_best[rec0 + c]);
+    for (int o = 16; o; o >>= 1) thr = fminf(thr, __shfl_xor_sync(0xffffffffu, thr, o));
     const int src = rows ? rows[row] : row;
     const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
     const float* cents = cb.centroids + (size_t)g * K * gd;
@@ -492,7 +504,7 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       uint32_t live = 0;
       int ix[kVqCap];
       int full_part = 0;
-      if (c < nchunk && w.rec_best[rec0 + c] <= thr) {
+      if (c < nchunk && w.rec_lmin[rec0 + c] <= thr) {
         const int m = w.rec_cnt[rec0 + c];
         if (m > kVqCap) {
           full_part = 1;
@@ -639,7 +651,7 @@ static cudaError_t vq_launch_gemm(const AstraCodebook& cb, const CUtensorMap& ta
       make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp, gdp,
                    BN / cluster, kBK, true))
     return cudaErrorInvalidValue;
-  VqEpilogue<BN> epi{Mg, K, nchunk, cb.c_sq, cb.c_norm_max, w};
+  VqEpilogue<BN> epi{Mg, K, nchunk, reinterpret_cast<const float4*>(cb.c_win), w};
   TileSched sched{(Mg + kBM - 1) / kBM, (K + BN - 1) / BN, G, 1};
   return cluster == 2 ? launch_tc_gemm<BN, 3, 3, 2>(ta, talo, tb, tblo, gdp, sched, Mg, K, epi, s,
                                                     num_sms())

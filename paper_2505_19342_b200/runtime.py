@@ -513,7 +513,8 @@ class AstraRuntime:
                      _p(self.qkv, 2 * D), 3 * D, _p(remote, 0 if remote is self.qkv else 0),
                      _p(remote, D), ld_r, self.key_src.data_ptr(), self.key_pos.data_ptr(),
                      self.segs.data_ptr(), self.n_segs, self.max_nq, self.H, self.dk,
-                     int(self.cfg.causal), int(self.fast), float(np.float32(1.0 / math.sqrt(self.dk))),
+                     2 if self.cfg.causal else 0,   # causal layouts hold prefix keys (layout.py)
+                     int(self.fast), float(np.float32(1.0 / math.sqrt(self.dk))),
                      None, self.o_hi.data_ptr(), _p(self.o_lo), D, R, R, remote.shape[0], s)
         # 6. h = stack + attn Wo
         whi, wlo = lay["wo"]

@@ -33,7 +33,8 @@ class _CB(ctypes.Structure):
     _fields_ = [("groups", ctypes.c_int), ("size", ctypes.c_int), ("group_dim", ctypes.c_int),
                 ("padded_dim", ctypes.c_int), ("centroids", ctypes.c_void_p),
                 ("c_hi", ctypes.c_void_p), ("c_lo", ctypes.c_void_p), ("c_sq", ctypes.c_void_p),
-                ("c_sq64", ctypes.c_void_p), ("c_norm_max", ctypes.c_void_p)]
+                ("c_sq64", ctypes.c_void_p), ("c_norm_max", ctypes.c_void_p),
+                ("c_win", ctypes.c_void_p)]
 
 
 class DeviceCodebook:
@@ -53,9 +54,10 @@ class DeviceCodebook:
         self.c_sq = torch.empty(g, k, dtype=torch.float32, device=dev)
         self.c_sq64 = torch.empty(g, k, dtype=torch.float64, device=dev)
         self.c_norm_max = torch.empty(g, dtype=torch.float32, device=dev)
+        self.c_win = torch.empty(g, k, 4, dtype=torch.float32, device=dev)
         self.struct = _CB(g, k, gd, self.padded_dim, self.centroids.data_ptr(), self.c_hi.data_ptr(),
                           self.c_lo.data_ptr(), self.c_sq.data_ptr(), self.c_sq64.data_ptr(),
-                          self.c_norm_max.data_ptr())
+                          self.c_norm_max.data_ptr(), self.c_win.data_ptr())
         _native.call("astra_vq_prepare", ctypes.byref(self.struct), _stream())
 
     @property

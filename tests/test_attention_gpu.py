@@ -208,3 +208,36 @@ def test_attention_fp32_parity_kernels_vs_fp64(cuda, spec, causal, force_simt):
     # fp32 accumulation — the same class as the parity-mode GEMMs
     assert err < 2e-5, err
     assert err_split < 2e-5, err_split
+
+
+@pytest.mark.parametrize("variant", [0, 2])
+@pytest.mark.parametrize("fp32", [False, True])
+def test_attention_causal_prefix_skip(cuda, variant, fp32):
+    """causal = 2 (prefix keys, the runtime's causal layout): key chunks past a query tile's
+    last position are skipped; results equal the masked reference."""
+    from paper_2505_19342_b200 import _native
+    heads, dk = 12, 64
+    spec = [(130, 300, 0), (64, 700, 0), (7, 7, 0), (300, 520, 0)]
+    qkv, table, segs_t, ks, kp, segs = _problem(99, spec, heads, dk, True,
+                                                dtype=torch.float32 if fp32 else torch.bfloat16)
+    D = heads * dk
+    out = torch.zeros(qkv.shape[0], D, dtype=torch.float32 if fp32 else torch.bfloat16,
+                      device="cuda")
+    _native.load().astra_attention_variant(variant)
+    es = qkv.element_size()
+    try:
+        _native.call("astra_attention", qkv.data_ptr(), 3 * D, qkv.data_ptr() + D * es,
+                     qkv.data_ptr() + 2 * D * es, 3 * D, table.data_ptr(),
+                     table.data_ptr() + D * es, 2 * D, ks.data_ptr(), kp.data_ptr(),
+                     segs_t.data_ptr(), len(segs), max(s[1] for s in segs), heads, dk, 2,
+                     0 if fp32 else 1, float(np.float32(1 / math.sqrt(dk))),
+                     out.data_ptr() if fp32 else None, None if fp32 else out.data_ptr(), None, D,
+                     qkv.shape[0], qkv.shape[0], table.shape[0],
+                     torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+    finally:
+        _native.load().astra_attention_variant(0)
+    ref = _reference(qkv, table, segs, ks, kp, heads, dk, True)
+    rows = torch.cat([torch.arange(s[0], s[0] + s[1]) for s in segs]).cuda()
+    err = (out.float()[rows] - ref[rows].float()).abs().max().item()
+    assert err < (1e-4 if fp32 else 2e-2), err
