@@ -25,6 +25,8 @@ __device__ __forceinline__ uint4* st_bf(uint8_t* stage, int r, int c) {    // c 
 }
 
 struct StdEpilogue {
+  static constexpr bool kStateful = false;
+  struct State {};
   int M, N;
   const float* bias;
   const float* residual;

@@ -55,6 +55,8 @@ struct TileCoord {
 struct TileSched {
   int num_m, num_n, num_b;
   int cluster;  // CTAs per cluster: 1, 2 (a pair along M) or 4 (two pairs along N)
+  int runs = 0;  // 1: a CTA (pair) takes a row block and ALL its column tiles in order (a "run"),
+                 // so a stateful epilogue can reduce across the columns of a row
   __device__ int cm() const { return cluster >= 2 ? 2 : 1; }
   __device__ int cn() const { return cluster == 4 ? 2 : 1; }
   __device__ int num_units_m() const { return (num_m + cm() - 1) / cm(); }
@@ -73,6 +75,39 @@ struct TileSched {
   }
 };
 
+// Tile sequence of one persistent CTA: tiles t = unit0, unit0 + units, ... (runs = 0: every
+// tile is a run of its own) or, with runs, row-block units rb = unit0, unit0 + units, ... each
+// followed through all its column tiles (t = rb * units_n + n).
+struct TileIter {
+  int t, n, un, rb, step, total, runs;
+  __device__ TileIter(const TileSched& s, int unit0, int units) {
+    un = s.num_units_n();
+    runs = s.runs;
+    step = units;
+    total = s.total();
+    rb = unit0;
+    n = 0;
+    t = runs ? rb * un : unit0;
+  }
+  __device__ bool valid() const { return t < total; }
+  __device__ bool first() const { return !runs || n == 0; }
+  __device__ bool last() const { return !runs || n == un - 1; }
+  __device__ void next() {
+    if (!runs) {
+      t += step;
+      return;
+    }
+    if (++n == un) {
+      n = 0;
+      rb += step;
+    }
+    t = rb * un + n;
+  }
+};
+
+// Epi::kStateful == false: stateless, per tile.  true: the epilogue keeps a per-thread
+// Epi::State across the tiles of a run (TileSched::runs) and is told the run's first / last
+// tile (e.g. the VQ argmin reducing a row over every code tile).
 // Epi must provide:
 //   __device__ void operator()(const TileCoord&, int row_in_tile /*0..127*/,
 //                              uint32_t tmem_row_addr /*lane-qualified TMEM address of col 0*/,
@@ -129,7 +164,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int pair_leader = rank & ~1;
   const int unit0 = blockIdx.x / CLUSTER, units = gridDim.x / CLUSTER;
   const int num_kb = (K + kBK - 1) / kBK;
-  const int total = sched.total();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -170,8 +204,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t full_pb = smem_u32(full_bar) & kPeerBitMask;   // multicast form
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = unit0; t < total; t += units) {
-        TileCoord tc = sched.get(t, rank);
+      for (TileIter it(sched, unit0, units); it.valid(); it.next()) {
+        TileCoord tc = sched.get(it.t, rank);
         const int arow = tc.batch * a_batch_rows + tc.m_blk * kBM;
         const int brow = tc.batch * b_batch_rows + tc.n_blk * BN + (kPair ? (rank & 1) * (BN / 2) : 0);
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -229,7 +263,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = unit0; t < total; t += units) {
+      for (TileIter it(sched, unit0, units); it.valid(); it.next()) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -295,12 +329,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t tempty0 = kPair ? mapa_shared(tempty_bar, pair_leader) : 0u;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = unit0; t < total; t += units) {
-      TileCoord tc = sched.get(t, rank);
+    typename Epi::State est{};
+    for (TileIter it(sched, unit0, units); it.valid(); it.next()) {
+      TileCoord tc = sched.get(it.t, rank);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;
-      if (!(dbg & 2)) epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage);
+      if constexpr (Epi::kStateful) {
+        epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage, est, it.first(), it.last());
+      } else {
+        if (!(dbg & 2)) epi(tc, row_in_tile, taddr, col_begin, col_end, part, stage);
+      }
       tc_fence_before();
       if (kPair) {
         __syncwarp();
@@ -373,7 +412,8 @@ inline cudaError_t launch_tc_gemm(const CUtensorMap& ta, const CUtensorMap& talo
               CLUSTER, n, sms);
   }
   const long max_units = max_clusters;
-  const int grid = (int)((total < max_units ? total : max_units) * CLUSTER);
+  const long work = sched.runs ? units_m * sched.num_b : total;   // runs: one unit per row block
+  const int grid = (int)((work < max_units ? work : max_units) * CLUSTER);
   cfg.gridDim = dim3(grid, 1, 1);
   return cudaLaunchKernelEx(&cfg, kern, ta, talo, tb, tblo, K, sched, a_batch_rows, b_batch_rows,
                             epi);

@@ -150,6 +150,8 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
   const int warps = blockDim.x >> 5;
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
+  // the re-rank list is appended to by the run-mode GEMM epilogue that follows: reset here
+  if (blockIdx.x == 0 && threadIdx.x == 0) *w.rr_count = 0;
   if (r >= M) return;
   const int src = rows ? rows[r] : r;
   const float* xr = x + (size_t)src * ldx;
@@ -173,6 +175,8 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
 // ---------------------------------------------------------- epilogue
 template <int BN>
 struct VqEpilogue {
+  static constexpr bool kStateful = false;
+  struct State {};
   int M, K, nchunk;         // nchunk = records per (g, row): kEpiParts per BN-code tile
   const float4* c_win;      // [G, K] {||c||^2, ||c||, eps ||c||^2, 0}
   VqWorkspace w;
@@ -249,6 +253,177 @@ struct VqEpilogue {
       w.rec_lmin[rec] = lmin;
       w.rec_cnt[rec] = cnt;
     }
+  }
+};
+
+// Grouped codebooks (G > 1): the GEMM runs in "runs" (TileSched::runs) — a CTA pair takes a
+// 128-row block of one group and sweeps every code tile of it — and this epilogue keeps each
+// (row, column part)'s window state in registers across the sweep, then merges the four parts
+// of the row through shared memory and DECIDES the row: one surviving candidate is written as
+// the index; several go to the fp64 re-rank list.  No per-chunk records, no finalize pass
+// (G = 16 at ViT-L: 16 records x 40 B per token-group were 190 MB of HBM traffic per layer).
+constexpr int kRunCap = 4;
+struct VqRunState {
+  float U, lmin;
+  int n, ovf;
+  int ci[kRunCap];
+  float cl[kRunCap];
+};
+
+template <int BN>
+struct VqRunEpilogue {
+  static constexpr bool kStateful = true;
+  using State = VqRunState;
+  int M, K;
+  const float4* c_win;      // [G, K] {||c||^2, ||c||, eps ||c||^2, 0}
+  VqWorkspace w;
+  int32_t* idx_out;         // [M, G]
+  int32_t* stats;           // nullable: stats[2] += window candidates
+  int G;
+
+  __device__ __forceinline__ void prune(State& st) const {
+    int k = 0;
+#pragma unroll
+    for (int i = 0; i < kRunCap; ++i)
+      if (i < st.n && st.cl[i] <= st.U) {
+        st.ci[k] = st.ci[i];
+        st.cl[k] = st.cl[i];
+        ++k;
+      }
+    st.n = k;
+  }
+
+  __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
+                                             int cb, int ce, int part, uint8_t* stage, State& st,
+                                             bool first, bool last) const {
+    const int row = tc.m_blk * kBM + row_in_tile;
+    const bool ok = row < M;
+    const int g = tc.batch;
+    const int col_base = tc.n_blk * BN;
+    const float4* cw = c_win + (size_t)g * K;
+    float4* scs = reinterpret_cast<float4*>(stage);
+    const int lane = threadIdx.x & 31;
+    const float xn = ok ? w.x_norm[(size_t)g * M + row] : 0.f;
+    const float a = window_a(xn);
+    if (first) {
+      st.U = INFINITY;
+      st.lmin = INFINITY;
+      st.n = 0;
+      st.ovf = 0;
+    }
+    // pass 1: this tile part's upper bound; the run's U only decreases
+    float ub[2] = {INFINITY, INFINITY};
+#pragma unroll 1
+    for (int c0 = cb; c0 < ce; c0 += 32) {
+      const int col0 = col_base + c0;
+      const float4 cl = (col0 + lane < K) ? __ldg(cw + col0 + lane)
+                                          : make_float4(INFINITY, 0.f, 0.f, 0.f);
+      uint32_t r[32];
+      tmem_ld32(taddr + c0, r);
+      tmem_ld_wait();
+      scs[lane] = cl;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float4 q = scs[j];
+        ub[j & 1] = fminf(ub[j & 1], fmaf(-2.0f, __uint_as_float(r[j]), q.x) + fmaf(a, q.y, q.z));
+      }
+      __syncwarp();
+    }
+    const float Ut = fminf(ub[0], ub[1]) + 1e-30f;
+    if (Ut < st.U) {
+      st.U = Ut;
+      prune(st);
+    }
+    // pass 2: candidates with L_k = s_k - D_k <= U
+#pragma unroll 1
+    for (int c0 = cb; c0 < ce; c0 += 32) {
+      const int col0 = col_base + c0;
+      const float4 cl = (col0 + lane < K) ? __ldg(cw + col0 + lane)
+                                          : make_float4(INFINITY, 0.f, 0.f, 0.f);
+      uint32_t r[32];
+      tmem_ld32(taddr + c0, r);
+      tmem_ld_wait();
+      scs[lane] = cl;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float4 q = scs[j];
+        const float lo = fmaf(-2.0f, __uint_as_float(r[j]), q.x) - fmaf(a, q.y, q.z);
+        st.lmin = fminf(st.lmin, lo);
+        if (lo <= st.U && col0 + j < K) {
+          if (st.n < kRunCap) {
+#pragma unroll
+            for (int i = 0; i < kRunCap; ++i)   // predicated: the state stays in registers
+              if (i == st.n) {
+                st.ci[i] = col0 + j;
+                st.cl[i] = lo;
+              }
+            ++st.n;
+          } else {
+            st.ovf = 1;
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (!last) return;
+    // ---- end of the run: merge the row's kEpiParts column parts (warps quarter + 4 p)
+    float* sh = reinterpret_cast<float*>(stage);          // [lane][12] words, this warp's part
+    float* my = sh + lane * 12;
+    __syncwarp();
+    my[0] = st.U;
+    my[1] = st.lmin;
+    reinterpret_cast<int*>(my)[2] = st.n;
+    reinterpret_cast<int*>(my)[3] = st.ovf;
+#pragma unroll
+    for (int i = 0; i < kRunCap; ++i) {
+      reinterpret_cast<int*>(my)[4 + i] = st.ci[i];
+      my[8 + i] = st.cl[i];
+    }
+    const int quarter = row_in_tile >> 5;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(32 * kEpiParts) : "memory");
+    if (part == 0 && ok) {
+      // stage areas of the warps of this quarter are kEpiStageBytes * 4 apart (warp + 4 p)
+      float U = INFINITY;
+#pragma unroll
+      for (int p = 0; p < kEpiParts; ++p) U = fminf(U, (sh + p * 4 * (kEpiStageBytes / 4))[lane * 12]);
+      int n = 0, only = 0x7FFFFFFF, ovf = 0, list[8];
+#pragma unroll
+      for (int p = 0; p < kEpiParts; ++p) {
+        const float* o = sh + p * 4 * (kEpiStageBytes / 4) + lane * 12;
+        if (o[1] > U) continue;                 // no code of this part can be the argmin
+        if (reinterpret_cast<const int*>(o)[3]) ovf = 1;
+        const int pn = reinterpret_cast<const int*>(o)[2];
+#pragma unroll
+        for (int i = 0; i < kRunCap; ++i)
+          if (i < pn && o[8 + i] <= U) {
+            const int k = reinterpret_cast<const int*>(o)[4 + i];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q == n) list[q] = k;
+            ++n;
+            only = min(only, k);
+          }
+      }
+      if (stats) atomicAdd(&stats[2], n);
+      if (n == 1 && !ovf) {
+        idx_out[(size_t)row * G + g] = only;
+      } else {
+        const int slot = atomicAdd(w.rr_count, 1);
+        int* ent = w.rr_list + (size_t)slot * kRREntry;
+        ent[0] = g * M + row;
+        if (!ovf && n >= 1 && n <= 8) {
+          ent[1] = n;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i < n) ent[2 + i] = list[i];
+        } else {
+          ent[1] = -2;                          // full fp64 scan of the group's codes
+        }
+      }
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(32 * kEpiParts) : "memory");
   }
 };
 
@@ -447,6 +622,29 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       if (lane == 0) {
         idx_out[(size_t)row * G + g] = bi;
         if (stats) atomicAdd(&stats[0], 1);
+      }
+      continue;
+    }
+    if (nd == -2) {
+      // run-mode overflow (grouped codebooks): exact fp64 scan of every code of the group
+      const int src = rows ? rows[row] : row;
+      const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
+      const float* cents = cb.centroids + (size_t)g * K * gd;
+      double pp = 0.0;
+      for (int e = lane; e < gd; e += 32) pp = fma((double)__ldg(xr + e), (double)__ldg(xr + e), pp);
+      pp = warp_sum_d(pp);
+      double bd = INFINITY;
+      int bi = -1;
+      for (int k = 0; k < K; ++k) {
+        const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cb.c_sq64[(size_t)g * K + k], lane);
+        if (d < bd) {   // ascending k: strict < keeps the lowest index on ties
+          bd = d;
+          bi = k;
+        }
+      }
+      if (lane == 0) {
+        idx_out[(size_t)row * G + g] = bi;
+        if (stats) atomicAdd(&stats[1], 1);
       }
       continue;
     }
@@ -659,10 +857,33 @@ static cudaError_t vq_launch_gemm(const AstraCodebook& cb, const CUtensorMap& ta
                                                     num_sms());
 }
 
+// Grouped codebooks: the run-mode GEMM (a CTA pair sweeps all code tiles of a row block)
+// decides every row in its epilogue; only multi-candidate rows reach the re-rank kernel.
+template <int BN>
+static cudaError_t vq_launch_run(const AstraCodebook& cb, const CUtensorMap& ta,
+                                 const CUtensorMap& talo, int M, VqWorkspace w, int32_t* idx_out,
+                                 int32_t* stats, int cluster, cudaStream_t s) {
+  const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
+  CUtensorMap tb, tblo;
+  if (make_tmap_2d(&tb, cb.c_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp, gdp,
+                   BN / cluster, kBK, true) ||
+      make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp, gdp,
+                   BN / cluster, kBK, true))
+    return cudaErrorInvalidValue;
+  VqRunEpilogue<BN> epi{M, K, reinterpret_cast<const float4*>(cb.c_win), w, idx_out, stats, G};
+  TileSched sched{(M + kBM - 1) / kBM, (K + BN - 1) / BN, G, 1};
+  sched.runs = 1;
+  return cluster == 2 ? launch_tc_gemm<BN, 3, 3, 2>(ta, talo, tb, tblo, gdp, sched, M, K, epi, s,
+                                                    num_sms())
+                      : launch_tc_gemm<BN, 3, 2, 1>(ta, talo, tb, tblo, gdp, sched, M, K, epi, s,
+                                                    num_sms());
+}
+
 // Distance GEMM + windowed-argmin epilogue over `Mg` operand rows (per group), then the
 // finalize over the M tokens.  rec_by_row: records are indexed by source row (pre-split
 // operands cover the whole stack) instead of by token.  Few token rows (one rank of a wide
-// split) take 128-code tiles so the persistent grid still covers the SMs.
+// split) take 128-code tiles so the persistent grid still covers the SMs.  Grouped codebooks
+// (G > 1, token-gathered operands) take the run-mode GEMM instead (no records, no finalize).
 static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const void* a_lo, int lda,
                             int Mg, VqWorkspace w, const float* x, int M, int ldx,
                             const int32_t* rows, int rec_by_row, int32_t* idx_out, int32_t* stats,
@@ -681,6 +902,18 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
   if ((st = make_tmap_2d(&talo, a_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * Mg, gdp,
                          lda, kBM, kBK, true)))
     return st;
+  if (G > 1 && !rec_by_row) {
+    const long runs = (long)G * ((Mg + kBM * cluster - 1) / (kBM * cluster));
+    const int rbn = (K <= kVqBNMin || runs * cluster < num_sms()) ? kVqBNMin : kVqBN;
+    const cudaError_t er = rbn == kVqBN
+        ? vq_launch_run<kVqBN>(cb, ta, talo, Mg, w, idx_out, stats, cluster, s)
+        : vq_launch_run<kVqBNMin>(cb, ta, talo, Mg, w, idx_out, stats, cluster, s);
+    ASTRA_CUDA_CHECK(er);
+    vq_rerank_kernel<<<num_sms() * 2, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
+                                                   Mg, rec_by_row, bn / kEpiParts);
+    ASTRA_CUDA_CHECK(cudaGetLastError());
+    return ASTRA_OK;
+  }
   const cudaError_t e = bn == kVqBN ? vq_launch_gemm<kVqBN>(cb, ta, talo, Mg, w, nchunk, cluster, s)
                                     : vq_launch_gemm<kVqBNMin>(cb, ta, talo, Mg, w, nchunk, cluster, s);
   ASTRA_CUDA_CHECK(e);
