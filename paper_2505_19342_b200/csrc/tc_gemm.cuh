@@ -332,6 +332,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     typename Epi::State est{};
     for (TileIter it(sched, unit0, units); it.valid(); it.next()) {
       TileCoord tc = sched.get(it.t, rank);
+      // stateful epilogues stage their per-tile inputs while the accumulator is still being
+      // computed (their global-load latency hides behind the wait)
+      if constexpr (Epi::kStateful) epi.pre(tc, row_in_tile, col_begin, col_end, part, stage, est, it.first());
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + acc * BN;

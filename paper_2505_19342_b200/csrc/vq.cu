@@ -172,6 +172,50 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
   }
 }
 
+// Vectorised form for unpadded groups (gd == gdp, gd % 4 == 0, gd/4 dividing or divisible by
+// 32): float4 loads, 8-byte hi/lo stores, per-group norms by a segmented shuffle reduction.
+// `per` = float4s per group; a warp covers 32 / per groups per step (per <= 32) or one group
+// in per / 32 steps.
+__global__ void vq_split_v4_kernel(const float* __restrict__ x, int M, int ldx,
+                                   const int32_t* __restrict__ rows, int G, int gd, VqWorkspace w) {
+  const int warps = blockDim.x >> 5;
+  const int r = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *w.rr_count = 0;
+  if (r >= M) return;
+  const int src = rows ? rows[r] : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * ldx);
+  const int per = gd >> 2;
+  auto put = [&](int g, int q, float4 v) {   // group g, float4 q of the group
+    __nv_bfloat16 h[4], l[4];
+    split_bf16(v.x, h[0], l[0]);
+    split_bf16(v.y, h[1], l[1]);
+    split_bf16(v.z, h[2], l[2]);
+    split_bf16(v.w, h[3], l[3]);
+    const size_t o = ((size_t)g * M + r) * gd + 4 * q;
+    *reinterpret_cast<uint2*>(w.x_hi + o) = *reinterpret_cast<const uint2*>(h);
+    *reinterpret_cast<uint2*>(w.x_lo + o) = *reinterpret_cast<const uint2*>(l);
+    return fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, v.w * v.w)));
+  };
+  if (per <= 32) {
+    const int gpi = 32 / per;
+    for (int g0 = 0; g0 < G; g0 += gpi) {
+      const int g = g0 + lane / per, q = lane % per;
+      float ss = 0.f;
+      if (g < G) ss = put(g, q, __ldg(xr + g * per + q));
+      for (int o = per >> 1; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (g < G && q == 0) w.x_norm[(size_t)g * M + r] = sqrtf(ss) * (1.0f + 1e-6f);
+    }
+  } else {
+    for (int g = 0; g < G; ++g) {
+      float ss = 0.f;
+      for (int q = lane; q < per; q += 32) ss += put(g, q, __ldg(xr + g * per + q));
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) w.x_norm[(size_t)g * M + r] = sqrtf(ss) * (1.0f + 1e-6f);
+    }
+  }
+}
+
 // ---------------------------------------------------------- epilogue
 template <int BN>
 struct VqEpilogue {
@@ -264,33 +308,99 @@ struct VqEpilogue {
 // (G = 16 at ViT-L: 16 records x 40 B per token-group were 190 MB of HBM traffic per layer).
 constexpr int kRunCap = 4;
 struct VqRunState {
-  float U, lmin;
-  int n, ovf;
-  int ci[kRunCap];
-  float cl[kRunCap];
+  float a, dmax2;   // the row's window slope (2 tau + 2 eps) ||x_g|| and 2 Dmax (run constants)
+  float U;       // min (s_k + D_k) over the codes examined in detail (only decreases)
+  float smin;    // min score s_k over every code swept so far
+  float ovl;     // smallest lower bound of a candidate dropped for want of a slot (+inf: none)
+  int n;         // live candidate slots (kept in the warp's stage smem, [slot][lane])
 };
 
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts_s32(uint32_t a, int v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float4 lds_v4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w) : "memory");
+}
+// r[j] for a run-time j in [0, 32): a 5-level select tree (keeps r in registers)
+__device__ __forceinline__ float pick32(const uint32_t (&r)[32], int j) {
+  float t16[16], t8[8], t4[4], t2[2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) t16[i] = __uint_as_float((j & 1) ? r[2 * i + 1] : r[2 * i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t8[i] = (j & 2) ? t16[2 * i + 1] : t16[2 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) t4[i] = (j & 4) ? t8[2 * i + 1] : t8[2 * i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) t2[i] = (j & 8) ? t4[2 * i + 1] : t4[2 * i];
+  return (j & 16) ? t2[1] : t2[0];
+}
+
+// Stage layout of one epilogue warp (kEpiStageBytes): [0, 1024) the window terms of the tile
+// part's (up to) 64 codes (float4 per code, broadcast reads), staged by pre() while the MMAs
+// run; [1024, 1536) candidate codes [kRunCap][32 lanes]; [1536, 2048) their lower bounds.  The
+// end-of-run merge reuses [0, 1536) as [lane][12] words.
+//
+// Filter (exact superset of the window test).  With D_k = a n_k + e_k <= Dmax (the group's max
+// code norm) and U' = min (s_k + D_k) over the codes examined in detail, a code with
+// s_k > smin + 2 Dmax has L_k = s_k - D_k > smin + Dmax >= (s + D) of the code holding smin
+// >= U' — never a candidate.  So the common path per score is one FFMA (s = ||c||^2 - 2 x.c)
+// and one FMNMX; only a 32-code chunk holding a score <= smin + 2 Dmax (a new running minimum
+// or a near tie; ~2-3 of a part's chunks per row) takes the per-code bounds.
 template <int BN>
 struct VqRunEpilogue {
   static constexpr bool kStateful = true;
   using State = VqRunState;
   int M, K;
   const float4* c_win;      // [G, K] {||c||^2, ||c||, eps ||c||^2, 0}
+  const float* c_norm_max;  // [G] max ||c|| (rounded up)
   VqWorkspace w;
   int32_t* idx_out;         // [M, G]
   int32_t* stats;           // nullable: stats[2] += window candidates
   int G;
 
-  __device__ __forceinline__ void prune(State& st) const {
-    int k = 0;
-#pragma unroll
-    for (int i = 0; i < kRunCap; ++i)
-      if (i < st.n && st.cl[i] <= st.U) {
-        st.ci[k] = st.ci[i];
-        st.cl[k] = st.cl[i];
-        ++k;
-      }
-    st.n = k;
+  // Before the tile's accumulator is ready: the window terms of this part's codes into smem
+  // and, on a run's first tile, the row's window constants.
+  __device__ __forceinline__ void pre(const TileCoord& tc, int row_in_tile, int cb, int ce,
+                                      int part, uint8_t* stage, State& st, bool first) const {
+    const int lane = threadIdx.x & 31;
+    const int g = tc.batch;
+    const int col0 = tc.n_blk * BN + cb + lane;
+    const float4* cw = c_win + (size_t)g * K;
+    const float4 c0 = col0 < K ? __ldg(cw + col0) : make_float4(INFINITY, 0.f, 0.f, 0.f);
+    const float4 c1 = (cb + 32 < ce && col0 + 32 < K) ? __ldg(cw + col0 + 32)
+                                                      : make_float4(INFINITY, 0.f, 0.f, 0.f);
+    if (first) {
+      const int row = tc.m_blk * kBM + row_in_tile;
+      const float xn = row < M ? w.x_norm[(size_t)g * M + row] : 0.f;
+      st.a = window_a(xn);
+      const float nmax = __ldg(c_norm_max + g);
+      st.dmax2 = 2.0f * (nmax * (st.a + kEps * nmax)) * (1.0f + 1e-6f);
+    }
+    const uint32_t s_scs = smem_u32(stage);
+    __syncwarp();   // the previous tile's reads of the staged terms are done
+    sts_v4(s_scs + 16 * lane, c0);
+    sts_v4(s_scs + 512 + 16 * lane, c1);
+    __syncwarp();
   }
 
   __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
@@ -300,86 +410,87 @@ struct VqRunEpilogue {
     const bool ok = row < M;
     const int g = tc.batch;
     const int col_base = tc.n_blk * BN;
-    const float4* cw = c_win + (size_t)g * K;
-    float4* scs = reinterpret_cast<float4*>(stage);
     const int lane = threadIdx.x & 31;
-    const float xn = ok ? w.x_norm[(size_t)g * M + row] : 0.f;
-    const float a = window_a(xn);
+    const uint32_t s_stage = smem_u32(stage), s_idx = s_stage + 1024 + 4 * lane,
+                   s_lo = s_stage + 1536 + 4 * lane;
+    const float a = st.a, dmax2 = st.dmax2;
     if (first) {
       st.U = INFINITY;
-      st.lmin = INFINITY;
+      st.smin = INFINITY;
+      st.ovl = INFINITY;
       st.n = 0;
-      st.ovf = 0;
     }
-    // pass 1: this tile part's upper bound; the run's U only decreases
-    float ub[2] = {INFINITY, INFINITY};
 #pragma unroll 1
     for (int c0 = cb; c0 < ce; c0 += 32) {
       const int col0 = col_base + c0;
-      const float4 cl = (col0 + lane < K) ? __ldg(cw + col0 + lane)
-                                          : make_float4(INFINITY, 0.f, 0.f, 0.f);
+      const uint32_t s_scs = s_stage + (c0 - cb) * 16;   // this chunk's 32 staged terms
       uint32_t r[32];
       tmem_ld32(taddr + c0, r);
       tmem_ld_wait();
-      scs[lane] = cl;
-      __syncwarp();
+      float m0 = INFINITY, m1 = INFINITY;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float4 q = scs[j];
-        ub[j & 1] = fminf(ub[j & 1], fmaf(-2.0f, __uint_as_float(r[j]), q.x) + fmaf(a, q.y, q.z));
+      for (int j = 0; j < 32; ++j) {   // r[j] <- s_j = ||c_j||^2 - 2 x.c_j
+        const float sc = fmaf(-2.0f, __uint_as_float(r[j]), lds_f32(s_scs + 16 * j));
+        r[j] = __float_as_uint(sc);
+        if (j & 1) m1 = fminf(m1, sc); else m0 = fminf(m0, sc);
       }
-      __syncwarp();
-    }
-    const float Ut = fminf(ub[0], ub[1]) + 1e-30f;
-    if (Ut < st.U) {
-      st.U = Ut;
-      prune(st);
-    }
-    // pass 2: candidates with L_k = s_k - D_k <= U
-#pragma unroll 1
-    for (int c0 = cb; c0 < ce; c0 += 32) {
-      const int col0 = col_base + c0;
-      const float4 cl = (col0 + lane < K) ? __ldg(cw + col0 + lane)
-                                          : make_float4(INFINITY, 0.f, 0.f, 0.f);
-      uint32_t r[32];
-      tmem_ld32(taddr + c0, r);
-      tmem_ld_wait();
-      scs[lane] = cl;
-      __syncwarp();
+      st.smin = fminf(st.smin, fminf(m0, m1));
+      // + a rounding margin of 2^-21 (|smin| + 2 Dmax): the comparisons stay exact supersets
+      const float thr = (st.smin + dmax2) + kEps * (fabsf(st.smin) + dmax2);
+      if (fminf(m0, m1) > thr) continue;   // common case: nothing in this chunk can compete
+      uint32_t m = 0;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float4 q = scs[j];
-        const float lo = fmaf(-2.0f, __uint_as_float(r[j]), q.x) - fmaf(a, q.y, q.z);
-        st.lmin = fminf(st.lmin, lo);
-        if (lo <= st.U && col0 + j < K) {
+      for (int j = 0; j < 32; ++j) m |= (__uint_as_float(r[j]) <= thr ? 1u : 0u) << j;
+      while (m) {
+        const int j = __ffs(m) - 1;
+        m &= m - 1;
+        const float sc = pick32(r, j);
+        const float4 q = lds_v4(s_scs + 16 * j);
+        const float d = fmaf(a, q.y, q.z);
+        const float up = sc + d + 1e-30f, lo = sc - d;
+        if (up < st.U) {   // tighter bound: prune the kept codes
+          st.U = up;
+          int k = 0;
+          for (int i = 0; i < st.n; ++i) {
+            const float li = lds_f32(s_lo + 128 * i);
+            if (li <= up) {
+              sts_f32(s_lo + 128 * k, li);
+              sts_s32(s_idx + 128 * k, lds_s32(s_idx + 128 * i));
+              ++k;
+            }
+          }
+          st.n = k;
+        }
+        if (lo <= st.U) {
           if (st.n < kRunCap) {
-#pragma unroll
-            for (int i = 0; i < kRunCap; ++i)   // predicated: the state stays in registers
-              if (i == st.n) {
-                st.ci[i] = col0 + j;
-                st.cl[i] = lo;
-              }
+            sts_s32(s_idx + 128 * st.n, col0 + j);
+            sts_f32(s_lo + 128 * st.n, lo);
             ++st.n;
           } else {
-            st.ovf = 1;
+            st.ovl = fminf(st.ovl, lo);
           }
         }
       }
-      __syncwarp();
     }
     if (!last) return;
     // ---- end of the run: merge the row's kEpiParts column parts (warps quarter + 4 p)
+    int ci[kRunCap];
+    float cl[kRunCap];
+#pragma unroll
+    for (int i = 0; i < kRunCap; ++i) {
+      ci[i] = i < st.n ? lds_s32(s_idx + 128 * i) : 0;
+      cl[i] = i < st.n ? lds_f32(s_lo + 128 * i) : INFINITY;
+    }
     float* sh = reinterpret_cast<float*>(stage);          // [lane][12] words, this warp's part
     float* my = sh + lane * 12;
     __syncwarp();
     my[0] = st.U;
-    my[1] = st.lmin;
+    my[1] = st.ovl;
     reinterpret_cast<int*>(my)[2] = st.n;
-    reinterpret_cast<int*>(my)[3] = st.ovf;
 #pragma unroll
     for (int i = 0; i < kRunCap; ++i) {
-      reinterpret_cast<int*>(my)[4 + i] = st.ci[i];
-      my[8 + i] = st.cl[i];
+      reinterpret_cast<int*>(my)[4 + i] = ci[i];
+      my[8 + i] = cl[i];
     }
     const int quarter = row_in_tile >> 5;
     asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(32 * kEpiParts) : "memory");
@@ -392,8 +503,7 @@ struct VqRunEpilogue {
 #pragma unroll
       for (int p = 0; p < kEpiParts; ++p) {
         const float* o = sh + p * 4 * (kEpiStageBytes / 4) + lane * 12;
-        if (o[1] > U) continue;                 // no code of this part can be the argmin
-        if (reinterpret_cast<const int*>(o)[3]) ovf = 1;
+        if (o[1] <= U) ovf = 1;                 // a dropped code is still a candidate
         const int pn = reinterpret_cast<const int*>(o)[2];
 #pragma unroll
         for (int i = 0; i < kRunCap; ++i)
@@ -551,6 +661,7 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
 // For group widths <= 1024 each lane loads its slice of the token and of a candidate row in
 // one batch of independent loads (one memory round trip per candidate, not one per 32
 // elements); a chunk whose candidate list overflowed contributes all of its 64 codes.
+template <bool kNarrow>
 __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const float* __restrict__ x,
                                                         int M, int ldx,
                                                         const int32_t* __restrict__ rows,
@@ -568,7 +679,45 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
     const int item = __shfl_sync(0xffffffffu, ev, 0);
     const int nd = __shfl_sync(0xffffffffu, ev, 1);
     const int g = item / M, row = item % M;
-    if (nd > 0 && cb.group_dim <= 1024) {
+    if (kNarrow && nd > 0) {
+      // narrow groups: lane q holds float4 q of the token slice; the slice and every candidate
+      // row load in one round trip, then one fp64 dot product per candidate
+      const int src = rows ? rows[row] : row;
+      const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * ldx + (size_t)g * gd);
+      const float4* cents = reinterpret_cast<const float4*>(cb.centroids + (size_t)g * K * gd);
+      const bool on = lane < (gd >> 2);
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 xv = on ? __ldg(xr + lane) : z;
+      int kk[kRRCands];
+      float4 cv[kRRCands];
+#pragma unroll
+      for (int i = 0; i < kRRCands; ++i) {
+        kk[i] = __shfl_sync(0xffffffffu, ev, 2 + min(i, nd - 1));
+        cv[i] = (on && i < nd) ? __ldg(cents + (size_t)kk[i] * (gd >> 2) + lane) : z;
+      }
+      double pp = fma((double)xv.x, (double)xv.x, fma((double)xv.y, (double)xv.y,
+                  fma((double)xv.z, (double)xv.z, (double)xv.w * (double)xv.w)));
+      pp = warp_sum_d(pp);
+      double bd = INFINITY;
+      int bi = -1;
+#pragma unroll
+      for (int i = 0; i < kRRCands; ++i) {
+        if (i >= nd) break;
+        double pc = fma((double)xv.x, (double)cv[i].x, fma((double)xv.y, (double)cv[i].y,
+                    fma((double)xv.z, (double)cv[i].z, (double)xv.w * (double)cv[i].w)));
+        const double d = (pp - 2.0 * warp_sum_d(pc)) + cb.c_sq64[(size_t)g * K + kk[i]];
+        if (d < bd || (d == bd && kk[i] < bi)) {
+          bd = d;
+          bi = kk[i];
+        }
+      }
+      if (lane == 0) {
+        idx_out[(size_t)row * G + g] = bi;
+        if (stats) atomicAdd(&stats[0], 1);
+      }
+      continue;
+    }
+    if (!kNarrow && nd > 0 && cb.group_dim <= 1024) {
       // direct: token slice and two candidate rows per round trip, fp64 dot products
       const int src = rows ? rows[row] : row;
       const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
@@ -626,7 +775,9 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       continue;
     }
     if (nd == -2) {
-      // run-mode overflow (grouped codebooks): exact fp64 scan of every code of the group
+      // run-mode overflow (grouped codebooks): exact fp64 scan of every code of the group, the
+      // lanes over the codes (lane k scores codes k, k + 32, ...; token slice broadcast from
+      // shared memory), then a lowest-index argmin across the warp
       const int src = rows ? rows[row] : row;
       const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
       const float* cents = cb.centroids + (size_t)g * K * gd;
@@ -634,12 +785,48 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       for (int e = lane; e < gd; e += 32) pp = fma((double)__ldg(xr + e), (double)__ldg(xr + e), pp);
       pp = warp_sum_d(pp);
       double bd = INFINITY;
-      int bi = -1;
-      for (int k = 0; k < K; ++k) {
-        const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cb.c_sq64[(size_t)g * K + k], lane);
-        if (d < bd) {   // ascending k: strict < keeps the lowest index on ties
-          bd = d;
-          bi = k;
+      int bi = 0x7FFFFFFF;
+      if (gd <= 32 * kVqCap) {
+        float* xsh = reinterpret_cast<float*>(s_cand[wib]);
+        for (int e = lane; e < gd; e += 32) xsh[e] = __ldg(xr + e);
+        __syncwarp();
+        for (int k = lane; k < K; k += 64) {   // codes k and k + 32 (independent chains)
+          const int k2 = min(k + 32, K - 1);
+          const float* c = cents + (size_t)k * gd;
+          const float* c2 = cents + (size_t)k2 * gd;
+          double pc = 0.0, pc2 = 0.0;
+          for (int e = 0; e < gd; ++e) {
+            const double xe = (double)xsh[e];
+            pc = fma(xe, (double)__ldg(c + e), pc);
+            pc2 = fma(xe, (double)__ldg(c2 + e), pc2);
+          }
+          const double d = (pp - 2.0 * pc) + cb.c_sq64[(size_t)g * K + k];
+          if (d < bd) {   // ascending k per lane: strict < keeps the lowest index
+            bd = d;
+            bi = k;
+          }
+          const double d2 = (pp - 2.0 * pc2) + cb.c_sq64[(size_t)g * K + k2];
+          if (k + 32 < K && d2 < bd) {
+            bd = d2;
+            bi = k2;
+          }
+        }
+        __syncwarp();
+        for (int o = 16; o; o >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const int ok_ = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (od < bd || (od == bd && ok_ < bi)) {
+            bd = od;
+            bi = ok_;
+          }
+        }
+      } else {
+        for (int k = 0; k < K; ++k) {
+          const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cb.c_sq64[(size_t)g * K + k], lane);
+          if (d < bd) {
+            bd = d;
+            bi = k;
+          }
         }
       }
       if (lane == 0) {
@@ -648,6 +835,7 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       }
       continue;
     }
+    if (kNarrow) continue;   // (run mode hands over direct lists and full scans only)
     const int rr = rec_by_row ? rows[row] : row;
     const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
     float thr = INFINITY;   // U: min over the chunks' upper bounds
@@ -870,7 +1058,8 @@ static cudaError_t vq_launch_run(const AstraCodebook& cb, const CUtensorMap& ta,
       make_tmap_2d(&tblo, cb.c_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp, gdp,
                    BN / cluster, kBK, true))
     return cudaErrorInvalidValue;
-  VqRunEpilogue<BN> epi{M, K, reinterpret_cast<const float4*>(cb.c_win), w, idx_out, stats, G};
+  VqRunEpilogue<BN> epi{M, K, reinterpret_cast<const float4*>(cb.c_win),
+                         reinterpret_cast<const float*>(cb.c_norm_max), w, idx_out, stats, G};
   TileSched sched{(M + kBM - 1) / kBM, (K + BN - 1) / BN, G, 1};
   sched.runs = 1;
   return cluster == 2 ? launch_tc_gemm<BN, 3, 3, 2>(ta, talo, tb, tblo, gdp, sched, M, K, epi, s,
@@ -909,8 +1098,13 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
         ? vq_launch_run<kVqBN>(cb, ta, talo, Mg, w, idx_out, stats, cluster, s)
         : vq_launch_run<kVqBNMin>(cb, ta, talo, Mg, w, idx_out, stats, cluster, s);
     ASTRA_CUDA_CHECK(er);
-    vq_rerank_kernel<<<num_sms() * 2, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
-                                                   Mg, rec_by_row, bn / kEpiParts);
+    const int gd = cb.group_dim;
+    if (gd <= 128 && gd % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0)
+      vq_rerank_kernel<true><<<num_sms() * 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
+                                                           stats, Mg, rec_by_row, bn / kEpiParts);
+    else
+      vq_rerank_kernel<false><<<num_sms() * 4, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
+                                                            stats, Mg, rec_by_row, bn / kEpiParts);
     ASTRA_CUDA_CHECK(cudaGetLastError());
     return ASTRA_OK;
   }
@@ -921,7 +1115,7 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
   vq_finalize_kernel<<<(items + 7) / 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                       stats, Mg, rec_by_row);
   ASTRA_CUDA_CHECK(cudaGetLastError());
-  vq_rerank_kernel<<<num_sms() * 2, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
+  vq_rerank_kernel<false><<<num_sms() * 4, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
                                                  Mg, rec_by_row, bn / kEpiParts);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -942,7 +1136,12 @@ extern "C" int astra_vq_encode(const AstraCodebook* cbp, const float* x, int M, 
   VqWorkspace w;
   carve(&w, workspace, M, G, K, gdp);
   cudaStream_t s = as_stream(stream);
-  vq_split_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, M, ldx, rows, G, cb.group_dim, gdp, w);
+  const int gd = cb.group_dim, per = gd / 4;
+  if (gd == gdp && gd % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      (per <= 32 ? 32 % per == 0 : per % 32 == 0))
+    vq_split_v4_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, M, ldx, rows, G, gd, w);
+  else
+    vq_split_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, M, ldx, rows, G, gd, gdp, w);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return vq_gemm_finalize(cb, w.x_hi, w.x_lo, gdp, M, w, x, M, ldx, rows, 0, idx_out, stats, s);
 }

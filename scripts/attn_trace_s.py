@@ -23,6 +23,9 @@ rt.forward()
 torch.cuda.synchronize()
 buf = torch.zeros(512 + 2 * 1024, dtype=torch.int64, device="cuda")
 lib = _native.load()
+lib.astra_attention_variant(2)
+rt.forward()
+torch.cuda.synchronize()
 lib.astra_attention_trace(buf.data_ptr())
 rt.forward()
 torch.cuda.synchronize()
