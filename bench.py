@@ -360,6 +360,11 @@ def _kernel_work(rt):
         # LN1 also writes the bf16 hi/lo split of the raw rows and their norms (VQ operand)
         "ln1": dict(flops=0, bytes=R * Dm * (4 + 2 + (4 if rt.presplit else 0)) + (R * 4 if rt.presplit else 0)),
         "ln2": dict(flops=0, bytes=R * Dm * (4 + 2)),
+        # N > 1, G > 1: received codes -> gathered codebook rows -> LN1 bf16 operand (fused), and
+        # the K|V projection of every received row
+        "decode_ln": dict(flops=0, bytes=rt.n_content_all * (G * 4 + Dm * 4 + Dm * ebf)),
+        "gemm_kv": dict(flops=2 * rt.n_content_all * 2 * Dm * Dm,
+                        bytes=(rt.n_content_all * Dm + 2 * Dm * Dm + rt.n_content_all * 2 * Dm) * 2),
     }
 
 

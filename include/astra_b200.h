@@ -116,6 +116,16 @@ int astra_vq_encode_split(const AstraCodebook* cb, const float* x, int ldx, cons
  * set *err_flag = 1 (caller maps it to IndexCorruptionError). */
 int astra_vq_decode(const AstraCodebook* cb, const int32_t* idx, int M, float* out, int ldo,
                     int32_t* err_flag, void* stream);
+/* VQ decode fused into LN1 — the K/V projection's A operand for received tokens of grouped
+ * codebooks (vq.dequantize vq.py:225-233 -> tensor.layer_norm tensor.py:318-345, as
+ * cluster._device_layer_compute does for every remote row, cluster.py:182-198): row m is gathered
+ * from the codebook rows idx[m, :] straight into registers, normalised in fp32 exactly like
+ * astra_layernorm, and written as bf16 hi[, lo] (pitch ld_bf).  The decoded fp32 row never
+ * reaches HBM.  Needs D = G * gd in {512, 768, 1024} and gd % 4 == 0.  Bad codes: *err_flag = 1,
+ * the row reads as zeros. */
+int astra_vq_decode_layernorm(const AstraCodebook* cb, const int32_t* idx, int M, const float* gain,
+                              const float* bias, float eps, void* out_hi, void* out_lo, int ld_bf,
+                              int32_t* err_flag, void* stream);
 
 /* ------------------------------------------------------- index wire format
  * The exchanged payload of allgather_indices (cluster.py:144-160; the

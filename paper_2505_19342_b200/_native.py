@@ -31,6 +31,8 @@ SIGNATURES: dict[str, list] = {
     "astra_vq_encode_workspace": [_c_int, _c_int, _c_int, _c_int],
     "astra_vq_encode": [_vp, _vp, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_ll, _vp],
     "astra_vq_decode": [_vp, _vp, _c_int, _vp, _c_int, _vp, _vp],
+    "astra_vq_decode_layernorm": [_vp, _vp, _c_int, _vp, _vp, ctypes.c_float, _vp, _vp, _c_int,
+                                  _vp, _vp],
     "astra_vq_encode_split_workspace": [_c_int, _c_int],
     "astra_vq_encode_split": [_vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp,
                               _vp, _vp, _c_ll, _vp],

@@ -12,6 +12,18 @@ namespace astra {
 
 // ---------------------------------------------------------------- LayerNorm
 // mean, biased variance, 1/sqrt(var + eps), affine — all fp32 like the reference.
+// Source rows of the LayerNorm: the stack itself, or (decode fused into LN1) the VQ decode of
+// received codes — row r, float4 q of the row = centroids[g][idx[r, g]][4q - g gd], a coalesced
+// gather of L2-resident codebook rows (vq.dequantize, vq.py:225-233, then tensor.layer_norm):
+// the decoded fp32 row never goes to HBM.  Codes outside [0, K) raise the error flag and read
+// as zero rows (the caller raises IndexCorruptionError, vq.py:229-231).
+struct LnGather {
+  const float* cents;     // [G, K, gd] fp32
+  const int32_t* idx;     // [M, G]
+  int G, K, gd;
+  int32_t* err;
+};
+
 template <int VPL>  // float4 vectors per lane (D = VPL * 128)
 __global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
                                  const float* __restrict__ gain, const float* __restrict__ bias,
@@ -19,17 +31,33 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
                                  __nv_bfloat16* __restrict__ out_hi, __nv_bfloat16* __restrict__ out_lo,
                                  int ld_bf, __nv_bfloat16* __restrict__ xs_hi,
                                  __nv_bfloat16* __restrict__ xs_lo, int ld_xs,
-                                 float* __restrict__ x_norm) {
+                                 float* __restrict__ x_norm, LnGather gat = LnGather{}) {
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   // one row per warp, every row of the grid in flight at once (no grid-stride tail: the
   // kernel is HBM-latency bound, and a second partial round doubles the exposed latency)
   const int row = blockIdx.x * warps + (threadIdx.x >> 5);
   if (row < M) {
-    const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * ldx);
     float4 v[VPL];
+    if (gat.cents) {
+      const int per = gat.gd >> 2;   // float4s per group
 #pragma unroll
-    for (int i = 0; i < VPL; ++i) v[i] = __ldg(xr + lane + 32 * i);
+      for (int i = 0; i < VPL; ++i) {
+        const int q = lane + 32 * i, g = q / per;
+        const int k = __ldg(gat.idx + (size_t)row * gat.G + g);
+        if (k < 0 || k >= gat.K) {
+          atomicExch(gat.err, 1);
+          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        } else {
+          v[i] = __ldg(reinterpret_cast<const float4*>(gat.cents + ((size_t)g * gat.K + k) * gat.gd) +
+                       (q - g * per));
+        }
+      }
+    } else {
+      const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * ldx);
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) v[i] = __ldg(xr + lane + 32 * i);
+    }
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
@@ -394,6 +422,38 @@ extern "C" int astra_layernorm_ex(const float* x, int M, int D, int ldx, const f
     layernorm_generic_kernel<<<grid, 256, 0, s>>>(x, M, D, ldx, gain, bias, eps, out_f32, ld_f32,
                                                   hi, lo, ld_bf);
   }
+  ASTRA_CUDA_CHECK(cudaGetLastError());
+  return ASTRA_OK;
+}
+
+extern "C" int astra_vq_decode_layernorm(const AstraCodebook* cbp, const int32_t* idx, int M,
+                                         const float* gain, const float* bias, float eps,
+                                         void* out_hi, void* out_lo, int ld_bf, int32_t* err_flag,
+                                         void* stream) {
+  ASTRA_REQUIRE(cbp && idx && gain && bias && out_hi && err_flag, ASTRA_ERR_SHAPE,
+                "decode_layernorm: null argument");
+  const AstraCodebook cb = *cbp;
+  const int D = cb.groups * cb.group_dim;
+  ASTRA_REQUIRE(M >= 0, ASTRA_ERR_SHAPE, "decode_layernorm: M < 0");
+  ASTRA_REQUIRE(eps > 0.f, ASTRA_ERR_SHAPE, "layer_norm: eps must be positive");
+  ASTRA_REQUIRE((D == 512 || D == 768 || D == 1024) && cb.group_dim % 4 == 0 && ld_bf % 4 == 0 &&
+                    (reinterpret_cast<uintptr_t>(cb.centroids) & 15) == 0,
+                ASTRA_ERR_SHAPE, "decode_layernorm: needs D in {512, 768, 1024} and D/G %% 4 == 0");
+  if (M == 0) return ASTRA_OK;
+  cudaStream_t s = as_stream(stream);
+  auto hi = reinterpret_cast<__nv_bfloat16*>(out_hi);
+  auto lo = reinterpret_cast<__nv_bfloat16*>(out_lo);
+  const LnGather gat{cb.centroids, idx, cb.groups, cb.size, cb.group_dim, err_flag};
+  const int grid1 = (M + 3) / 4;
+  if (D == 768)
+    layernorm_kernel<6><<<grid1, 128, 0, s>>>(nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
+                                             ld_bf, nullptr, nullptr, 0, nullptr, gat);
+  else if (D == 1024)
+    layernorm_kernel<8><<<grid1, 128, 0, s>>>(nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
+                                             ld_bf, nullptr, nullptr, 0, nullptr, gat);
+  else
+    layernorm_kernel<4><<<grid1, 128, 0, s>>>(nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
+                                             ld_bf, nullptr, nullptr, 0, nullptr, gat);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }

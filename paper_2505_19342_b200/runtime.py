@@ -252,6 +252,11 @@ class AstraRuntime:
         _native.call("astra_layernorm", x_f32.data_ptr(), m, D, x_f32.stride(0),
                      lay["ln1_g"].data_ptr(), lay["ln1_b"].data_ptr(), LN_EPS, None, 0,
                      ln_hi.data_ptr(), _p(ln_lo), D, _stream())
+        self._kv_gemm(lay, m, out, ln_hi, ln_lo)
+
+    def _kv_gemm(self, lay, m: int, out: torch.Tensor, ln_hi, ln_lo):
+        """[Wk;Wv] projection of m LN1 rows (bf16 hi[, lo]) into out [m, 2D]."""
+        D = self.D
         whi, wlo = lay["wqkv"]
         kernels.gemm(ln_hi[:m], whi[D:], a_lo=None if ln_lo is None else ln_lo[:m],
                      b_lo=None if wlo is None else wlo[D:],
@@ -315,7 +320,11 @@ class AstraRuntime:
             self.gofs_dev = torch.tensor(np.asarray(self.gofs, dtype=np.int32), device=dev)
         if self.has_remote and self.G > 1:
             n = self.n_content_all
-            self.xhat = e(n, D)
+            gd = D // self.G
+            # decode fused into LN1 when the vector LN kernel covers the width (else decode ->
+            # fp32 rows -> LN1); fused_decode = False is the A/B switch for the bench script
+            self.fused_decode = D in (512, 768, 1024) and gd % 4 == 0
+            self.xhat = None if self.fused_decode else e(n, D)
             self.hat_hi = e(n, D, dt=BF16)
             self.hat_lo = None if self.fast else e(n, D, dt=BF16)
             self.kvhat = e(n, 2 * D, dt=BF16 if self.fast else torch.float32)
@@ -486,8 +495,21 @@ class AstraRuntime:
                                  self.idx_all.data_ptr(), self.key_src.data_ptr(), s)
                 remote = lay["kvtab"]
             else:
-                cb.decode(self.idx_all, out=self.xhat, err=self.dec_err)
-                self._kv_rows(lay, self.xhat, self.kvhat, self.hat_hi, self.hat_lo)
+                with self._op("decode_ln"):
+                    if self.fused_decode:
+                        # decode fused into LN1: received codes -> LN1(C[idx]) as the K|V
+                        # projection's bf16 operand, no fp32 decoded rows in HBM
+                        _native.call("astra_vq_decode_layernorm", ctypes.byref(cb.struct),
+                                     self.idx_all.data_ptr(), self.n_content_all,
+                                     lay["ln1_g"].data_ptr(), lay["ln1_b"].data_ptr(), LN_EPS,
+                                     self.hat_hi.data_ptr(), _p(self.hat_lo), D, self.dec_err.data_ptr(), s)
+                    else:
+                        cb.decode(self.idx_all, out=self.xhat, err=self.dec_err)
+                        _native.call("astra_layernorm", self.xhat.data_ptr(), self.n_content_all, D, D,
+                                     lay["ln1_g"].data_ptr(), lay["ln1_b"].data_ptr(), LN_EPS, None, 0,
+                                     self.hat_hi.data_ptr(), _p(self.hat_lo), D, s)
+                with self._op("gemm_kv"):
+                    self._kv_gemm(lay, self.n_content_all, self.kvhat, self.hat_hi, self.hat_lo)
                 remote = self.kvhat
         else:
             remote = self.qkv

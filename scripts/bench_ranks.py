@@ -24,6 +24,7 @@ CONFIGS = {
     "vitb": (12, 768, 12, 1000, 196, 64, 1024, 1, False),
     "gpt2s": (12, 768, 12, 50257, 1024, 4, 1024, 1, True),
     "vitl": (24, 1024, 16, 1000, 576, 32, 1024, 1, False),
+    "vitl_g16": (24, 1024, 16, 1000, 576, 32, 1024, 16, False),
     "vitl_g32": (24, 1024, 16, 1000, 576, 32, 1024, 32, False),
 }
 

@@ -146,3 +146,30 @@ def test_cuda_graph_replay_matches_eager(cuda):
     rt.stage_input(xs)
     rt.graph.replay()
     np.testing.assert_array_equal(rt.logits.cpu().numpy(), eager)
+
+
+@pytest.mark.parametrize("precision,tol", [("parity", 1e-4), ("fast", 3e-2)])
+def test_grouped_remote_rows_fused_decode_vs_oracle(cuda, precision, tol):
+    """G = 16 codebooks at ViT-B width, N = 4: the received rows go through the fused decode+LN1
+    kernel and the K|V GEMM; logits match the oracle's run_inference on the same codebooks."""
+    from paper_2505_19342_b200 import cluster, model, vq
+    from paper_2505_19342_b200.runtime import AstraRuntime
+    cfg = model.ModelConfig(layers=2, hidden=768, heads=12, vocab_or_classes=10, max_tokens=65,
+                            causal=False, codebook_size=64, groups=16)
+    params = model.init_params(cfg, seed=2)
+    ocfg = O.Config(layers=2, hidden=768, heads=12, vocab_or_classes=10, max_tokens=65,
+                    causal=False, codebook_size=64, groups=16)
+    op = O.init_params(ocfg, seed=2)
+    xs, _ = O.make_classify_data(768, 64, 3, seed=5, task_seed=0)
+    O.initialize_codebooks(op, xs[:2], "classify", seed=0, iterations=4)
+    for i, b in enumerate(params.blocks):
+        b.codebook = vq.Codebook(layer_id=i, groups=16, centroids=op.codebooks[i])
+    plan = cluster.partition_tokens(64, 4)
+    rt = AstraRuntime(params, plan, batch=1, precision=precision)
+    assert rt.fused_decode
+    x = xs[2]
+    got = np.asarray(rt.classify_numpy(x[None])).reshape(-1)
+    want = np.asarray(O.run_inference(op, O.partition_tokens(64, 4), x).output).reshape(-1)
+    err = np.abs(got - want).max()
+    assert err <= tol, err
+    assert int(np.argmax(got)) == int(np.argmax(want))

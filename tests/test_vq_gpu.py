@@ -97,3 +97,40 @@ def test_pack_roundtrip(cuda, bits, n):
         bad = kernels.unpack_indices(words, n, bits, int(idx.max()), err=err)
         assert int(err.item()) == 1
         del bad
+
+
+@pytest.mark.parametrize("m,k,d,g", [(3000, 1024, 768, 16), (777, 256, 1024, 16), (500, 64, 512, 2),
+                                     (300, 32, 768, 32)])
+def test_decode_layernorm_equals_decode_then_layernorm(cuda, m, k, d, g):
+    """astra_vq_decode_layernorm (decode fused into LN1) is bitwise the two-kernel path, in both
+    the fast (bf16) and the parity (bf16 hi/lo) operand forms; bad codes raise the flag."""
+    from paper_2505_19342_b200 import _native
+    from paper_2505_19342_b200.vq import DeviceCodebook
+    import ctypes
+    rng = np.random.default_rng(m + d)
+    gd = d // g
+    cents = torch.from_numpy(rng.normal(size=(g, k, gd)).astype(np.float32)).to(cuda)
+    cb = DeviceCodebook(cents)
+    idx = torch.from_numpy(rng.integers(0, k, size=(m, g)).astype(np.int32)).to(cuda)
+    gain = torch.from_numpy(rng.normal(size=d).astype(np.float32)).to(cuda)
+    bias = torch.from_numpy(rng.normal(size=d).astype(np.float32)).to(cuda)
+    s = torch.cuda.current_stream().cuda_stream
+    err = torch.zeros(2, dtype=torch.int32, device=cuda)
+    xhat = cb.decode(idx)
+    want_hi = torch.empty(m, d, dtype=torch.bfloat16, device=cuda)
+    want_lo = torch.empty_like(want_hi)
+    _native.call("astra_layernorm", xhat.data_ptr(), m, d, d, gain.data_ptr(), bias.data_ptr(),
+                 1e-5, None, 0, want_hi.data_ptr(), want_lo.data_ptr(), d, s)
+    hi, lo = torch.empty_like(want_hi), torch.empty_like(want_lo)
+    _native.call("astra_vq_decode_layernorm", ctypes.byref(cb.struct), idx.data_ptr(), m,
+                 gain.data_ptr(), bias.data_ptr(), 1e-5, hi.data_ptr(), lo.data_ptr(), d,
+                 err.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert int(err[0]) == 0
+    assert torch.equal(hi.view(torch.int16), want_hi.view(torch.int16))
+    assert torch.equal(lo.view(torch.int16), want_lo.view(torch.int16))
+    idx[m // 2, g - 1] = k   # out of range
+    _native.call("astra_vq_decode_layernorm", ctypes.byref(cb.struct), idx.data_ptr(), m,
+                 gain.data_ptr(), bias.data_ptr(), 1e-5, hi.data_ptr(), None, d, err.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert int(err[0]) == 1
