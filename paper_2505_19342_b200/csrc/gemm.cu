@@ -24,9 +24,25 @@ __device__ __forceinline__ uint4* st_bf(uint8_t* stage, int r, int c) {    // c 
   return reinterpret_cast<uint4*>(stage + r * 32 + ((c ^ ((r >> 2) & 1)) << 4));
 }
 
-struct StdEpilogue {
-  static constexpr bool kStateful = false;
-  struct State {};
+// Epilogue flags: 0 = generic (the pointers / gelu field decide at run time); otherwise a
+// compile-time specialisation for the block's hot GEMMs (no dead branches, no lo split when the
+// output is bf16 only) — the W1 epilogue was instruction-bound at ~27 instructions per output.
+constexpr int kEpBias = 1, kEpGeluFast = 2, kEpGeluExact = 4, kEpResid = 8, kEpF32 = 16,
+              kEpHi = 32, kEpLo = 64;
+
+template <int kF>
+struct StdEpilogueT {
+  // Stateful only to carry the residual prefetch: the warp's slice of the next 16-column
+  // residual chunk (4 rows x 16 B per lane) is loaded one chunk ahead, and the first chunk of a
+  // tile in pre(), before the accumulator is ready — the Wo / W2 epilogues stream 77 MB of
+  // fp32 residual per launch, and one exposed HBM round trip per chunk left the per-SM
+  // bandwidth share two-thirds idle.
+  static constexpr bool kStateful = true;
+  // (the generic form keeps the synchronous residual load: the prefetch registers made it spill)
+  static constexpr bool kPrefetch = (kF & kEpResid) != 0;
+  struct State {
+    float4 res[kPrefetch ? 4 : 1];
+  };
   int M, N;
   const float* bias;
   const float* residual;
@@ -55,8 +71,38 @@ struct StdEpilogue {
     __syncwarp();
   }
 
+  // residual slice of the chunk at col0 for this lane: rows row0 + 8 i + lane / 4, 16 B chunk
+  // lane % 4 (the coalesced pattern the staging tile transposes)
+  __device__ __forceinline__ void load_res(float4 (&res)[kPrefetch ? 4 : 1], int row0, int col0) const {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < (kPrefetch ? 4 : 1); ++i) {
+      const int grow = row0 + i * 8 + (lane >> 2);
+      res[i] = grow < M ? __ldg(reinterpret_cast<const float4*>(residual + (size_t)grow * ld_res + col0) +
+                                (lane & 3))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+
+  __device__ __forceinline__ void pre(const TileCoord& tc, int row_in_tile, int cb, int /*ce*/,
+                                      int /*part*/, uint8_t* /*stage*/, State& st,
+                                      bool /*first*/) const {
+    const int col0 = tc.n_blk * BN + cb;
+    if (kPrefetch && col0 + 16 <= N)
+      load_res(st.res, tc.m_blk * kBM + row_in_tile - (threadIdx.x & 31), col0);
+  }
+
   __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
-                                             int cb, int ce, int /*part*/, uint8_t* stage) const {
+                                             int cb, int ce, int /*part*/, uint8_t* stage,
+                                             State& st, bool /*first*/, bool /*last*/) const {
+    if (g_gemm_debug & 2) return;   // bench-only isolation switch (tc_gemm.cuh)
+    const bool has_bias = kF ? bool(kF & kEpBias) : bias != nullptr;
+    const int gmode = kF ? ((kF & kEpGeluFast) ? 2 : (kF & kEpGeluExact) ? 1 : 0) : gelu;
+    const bool has_res = kF ? bool(kF & kEpResid) : residual != nullptr;
+    const bool has_f32 = kF ? bool(kF & kEpF32) : out_f32 != nullptr;
+    const bool has_hi = kF ? bool(kF & kEpHi) : out_hi != nullptr;
+    const bool has_lo = kF ? bool(kF & kEpLo) : out_lo != nullptr;
+    const bool vec_ok = kF ? true : vec != 0;
     const int lane = threadIdx.x & 31;
     const int row0 = tc.m_blk * kBM + row_in_tile - lane;  // first row of this warp's slab
     const int row = row0 + lane;
@@ -66,17 +112,17 @@ struct StdEpilogue {
     for (int c0 = cb; c0 < ce; c0 += 16) {
       const int col0 = tc.n_blk * BN + c0;
       // one coalesced bias load per warp, issued before the TMEM load so the latencies overlap
-      const float bl = (bias && lane < 16 && col0 + lane < N) ? __ldg(bias + col0 + lane) : 0.f;
+      const float bl = (has_bias && lane < 16 && col0 + lane < N) ? __ldg(bias + col0 + lane) : 0.f;
       uint32_t r[16];
       tmem_ld16(taddr + c0, r);
       tmem_ld_wait();
       if (col0 >= N) continue;  // warp-uniform
       const bool full = (col0 + 16 <= N);
-      const bool fast = full && vec;
+      const bool fast = full && vec_ok;
       float v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-      if (bias) {
+      if (has_bias) {
         if (lane < 16) sbias[lane] = bl;
         __syncwarp();
 #pragma unroll
@@ -89,21 +135,54 @@ struct StdEpilogue {
         }
         __syncwarp();
       }
-      if (gelu == 1) {
+      if (gmode == 1) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = gelu_erf(v[j]);
-      } else if (gelu == 2) {
+      } else if (gmode == 2) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = gelu_erf_bf16(v[j]);
       }
-      if (residual) {
+      if constexpr (kPrefetch && (kF & kEpF32) && !(kF & kEpHi)) {
         if (fast) {
+          // residual + fp32 output in the coalesced layout: one smem transpose of the
+          // accumulator, then out = residual + acc per 16-byte chunk (the residual of this
+          // chunk arrived with the previous one; the next chunk's loads go out first)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            *st_f32(stage, lane, c) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          float4 rv[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rv[i] = st.res[i];
+          if (c0 + 16 < ce && col0 + 32 <= N) load_res(st.res, row0, col0 + 16);
+          __syncwarp();
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int rr = i * 8 + (lane >> 2), ch = lane & 3, grow = row0 + rr;
+            const float4 a = *st_f32(stage, rr, ch);
             if (grow < M)
-              *st_f32(stage, rr, ch) =
-                  __ldg(reinterpret_cast<const float4*>(residual + (size_t)grow * ld_res + col0) + ch);
+              *(reinterpret_cast<float4*>(out_f32 + (size_t)grow * ld_f32 + col0) + ch) =
+                  make_float4(rv[i].x + a.x, rv[i].y + a.y, rv[i].z + a.z, rv[i].w + a.w);
+          }
+          __syncwarp();
+          continue;
+        }
+      }
+      if (has_res) {
+        if (fast) {
+          if constexpr (kPrefetch) {
+            // this chunk's residual arrived with the previous chunk (or pre()); the next
+            // chunk's loads go out before this one is consumed
+#pragma unroll
+            for (int i = 0; i < 4; ++i) *st_f32(stage, i * 8 + (lane >> 2), lane & 3) = st.res[i];
+            if (c0 + 16 < ce && col0 + 32 <= N) load_res(st.res, row0, col0 + 16);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int rr = i * 8 + (lane >> 2), ch = lane & 3, grow = row0 + rr;
+              if (grow < M)
+                *st_f32(stage, rr, ch) =
+                    __ldg(reinterpret_cast<const float4*>(residual + (size_t)grow * ld_res + col0) + ch);
+            }
           }
           __syncwarp();
 #pragma unroll
@@ -121,7 +200,7 @@ struct StdEpilogue {
             if (col0 + j < N) v[j] = rp[j] + v[j];
         }
       }
-      if (out_f32) {
+      if (has_f32) {
         if (fast) {
 #pragma unroll
           for (int c = 0; c < 4; ++c)
@@ -141,21 +220,23 @@ struct StdEpilogue {
             if (col0 + j < N) op[j] = v[j];
         }
       }
-      if (out_hi) {
+      if (has_hi) {
         uint32_t hp[8], lp[8];
 #pragma unroll
         for (int j = 0; j < 16; j += 2) {
           __nv_bfloat162 h2 = __floats2bfloat162_rn(v[j], v[j + 1]);
-          __nv_bfloat162 l2 = __floats2bfloat162_rn(v[j] - __low2float(h2), v[j + 1] - __high2float(h2));
           hp[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
-          lp[j >> 1] = *reinterpret_cast<uint32_t*>(&l2);
+          if (has_lo) {
+            __nv_bfloat162 l2 = __floats2bfloat162_rn(v[j] - __low2float(h2), v[j + 1] - __high2float(h2));
+            lp[j >> 1] = *reinterpret_cast<uint32_t*>(&l2);
+          }
         }
         if (fast) {
           store_bf16(stage, out_hi, row0, col0, hp);
-          if (out_lo) store_bf16(stage, out_lo, row0, col0, lp);
+          if (has_lo) store_bf16(stage, out_lo, row0, col0, lp);
         } else if (row_ok) {
           __nv_bfloat16* hq = out_hi + (size_t)row * ld_bf + col0;
-          __nv_bfloat16* lq = out_lo ? out_lo + (size_t)row * ld_bf + col0 : nullptr;
+          __nv_bfloat16* lq = has_lo ? out_lo + (size_t)row * ld_bf + col0 : nullptr;
           const __nv_bfloat16* hs = reinterpret_cast<const __nv_bfloat16*>(hp);
           const __nv_bfloat16* ls = reinterpret_cast<const __nv_bfloat16*>(lp);
           for (int j = 0; j < 16; ++j)
@@ -169,6 +250,8 @@ struct StdEpilogue {
   }
 };
 
+using StdEpilogue = StdEpilogueT<0>;
+
 // Deepest operand ring that fits next to the epilogue staging (<= 192 KB of stages).
 template <int BN, int PASSES, int CLUSTER>
 constexpr int gemm_stages() {
@@ -177,9 +260,9 @@ constexpr int gemm_stages() {
   return n > 8 ? 8 : n;
 }
 
-template <int BN, int PASSES>
+template <int BN, int PASSES, class Epi>
 static int launch_std(const CUtensorMap& ta, const CUtensorMap& talo, const CUtensorMap& tb,
-                      const CUtensorMap& tblo, int M, int N, int K, StdEpilogue epi,
+                      const CUtensorMap& tblo, int M, int N, int K, Epi epi,
                       cudaStream_t stream, int cluster) {
   TileSched sched{(M + kBM - 1) / kBM, (N + BN - 1) / BN, 1, 1};
   epi.BN = BN;
@@ -190,6 +273,23 @@ static int launch_std(const CUtensorMap& ta, const CUtensorMap& talo, const CUte
                          ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms())
                      : launch_tc_gemm<BN, PASSES, gemm_stages<BN, PASSES, 1>(), 1>(
                          ta, talo, tb, tblo, K, sched, 0, 0, epi, stream, num_sms());
+  ASTRA_CUDA_CHECK(e);
+  return ASTRA_OK;
+}
+
+// A compile-time-specialised epilogue for the hot fast-mode GEMMs (CTA pairs, 1 pass).
+template <int kF>
+static int launch_spec(int BN, const CUtensorMap& ta, const CUtensorMap& talo,
+                       const CUtensorMap& tb, const CUtensorMap& tblo, int M, int N, int K,
+                       const StdEpilogue& g, cudaStream_t stream) {
+  StdEpilogueT<kF> epi{g.M, g.N, g.bias, g.residual, g.ld_res, g.out_f32, g.ld_f32, g.out_hi,
+                       g.out_lo, g.ld_bf, g.gelu, BN, g.vec};
+  TileSched sched{(M + kBM - 1) / kBM, (N + BN - 1) / BN, 1, 1};
+  const cudaError_t e =
+      BN == 256 ? launch_tc_gemm<256, 1, gemm_stages<256, 1, 2>(), 2>(ta, talo, tb, tblo, K, sched,
+                                                                      0, 0, epi, stream, num_sms())
+                : launch_tc_gemm<192, 1, gemm_stages<192, 1, 2>(), 2>(ta, talo, tb, tblo, K, sched,
+                                                                      0, 0, epi, stream, num_sms());
   ASTRA_CUDA_CHECK(e);
   return ASTRA_OK;
 }
@@ -339,6 +439,26 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                   ld_f32, reinterpret_cast<__nv_bfloat16*>(out_hi),
                   reinterpret_cast<__nv_bfloat16*>(out_lo), ld_bf, gelu, 0, vec};
   cudaStream_t s = as_stream(stream);
+  if (passes == 1 && cluster == 2 && vec && (BN == 256 || BN == 192)) {
+    const int flags = (bias ? kEpBias : 0) | (gelu == 2 ? kEpGeluFast : 0) |
+                      (gelu == 1 ? kEpGeluExact : 0) | (residual ? kEpResid : 0) |
+                      (out_f32 ? kEpF32 : 0) | (out_hi ? kEpHi : 0) | (out_lo ? kEpLo : 0);
+    int st2 = -1;
+    switch (flags) {   // the fast-mode block GEMMs: Q|K|V, W1, Wo, W2
+      case kEpHi: st2 = launch_spec<kEpHi>(BN, ta, talo, tb, tblo, M, N, K, epi, s); break;
+      case kEpBias | kEpGeluFast | kEpHi:
+        st2 = launch_spec<kEpBias | kEpGeluFast | kEpHi>(BN, ta, talo, tb, tblo, M, N, K, epi, s);
+        break;
+      case kEpResid | kEpF32:
+        st2 = launch_spec<kEpResid | kEpF32>(BN, ta, talo, tb, tblo, M, N, K, epi, s);
+        break;
+      case kEpBias | kEpResid | kEpF32:
+        st2 = launch_spec<kEpBias | kEpResid | kEpF32>(BN, ta, talo, tb, tblo, M, N, K, epi, s);
+        break;
+      default: break;
+    }
+    if (st2 >= 0) return st2;
+  }
   if (passes == 1) {
     if (BN == 256) return launch_std<256, 1>(ta, talo, tb, tblo, M, N, K, epi, s, cluster);  // 230 KB
     if (BN == 192) return launch_std<192, 1>(ta, talo, tb, tblo, M, N, K, epi, s, cluster);
