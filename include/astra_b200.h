@@ -109,6 +109,16 @@ int astra_vq_encode_split(const AstraCodebook* cb, const float* x, int ldx, cons
                           const void* x_lo, int ld_split, const float* x_norm, int R,
                           const int32_t* rows, int M, int32_t* idx_out, int32_t* stats,
                           void* workspace, int64_t workspace_bytes, void* stream);
+/* Same, with row_token [R] = the token index of stack row r (-1: not a token row; the inverse
+ * of rows), precomputed by the caller.  When the stack has at least as many 256-row blocks as
+ * the GPU has CTA pairs, the distance GEMM runs in run mode (a CTA pair sweeps the whole
+ * codebook for its rows and decides them in the epilogue; no finalize pass) and uses the map
+ * instead of rebuilding it. */
+int astra_vq_encode_split_ex(const AstraCodebook* cb, const float* x, int ldx, const void* x_hi,
+                             const void* x_lo, int ld_split, const float* x_norm, int R,
+                             const int32_t* rows, int M, const int32_t* row_token,
+                             int32_t* idx_out, int32_t* stats, void* workspace,
+                             int64_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------ VQ decode
  * Replaces vq.dequantize (vq.py:225-233): out[m, g*gd:(g+1)*gd] =

@@ -36,6 +36,8 @@ SIGNATURES: dict[str, list] = {
     "astra_vq_encode_split_workspace": [_c_int, _c_int],
     "astra_vq_encode_split": [_vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp,
                               _vp, _vp, _c_ll, _vp],
+    "astra_vq_encode_split_ex": [_vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _c_int, _vp, _c_int, _vp,
+                                 _vp, _vp, _vp, _c_ll, _vp],
     "astra_layernorm_ex": [_vp, _c_int, _c_int, _c_int, _vp, _vp, ctypes.c_float, _vp, _c_int,
                            _vp, _vp, _c_int, _vp, _vp, _c_int, _vp, _vp],
     "astra_pack_indices": [_vp, _c_int, _c_int, _vp, _vp],
@@ -114,7 +116,8 @@ def check(status: int, what: str = "") -> None:
 
 
 # kernels each C-ABI call enqueues (for launch accounting in bench.py)
-LAUNCHES = {"astra_vq_encode": 3, "astra_vq_prepare": 2, "astra_vq_encode_split": 3}
+LAUNCHES = {"astra_vq_encode": 3, "astra_vq_prepare": 2, "astra_vq_encode_split": 3,
+            "astra_vq_encode_split_ex": 3}
 _counter: dict | None = None
 
 

@@ -22,6 +22,8 @@
 // that plus fp32 rounding of the epilogue arithmetic — bounded PER CODE with ||c_k|| (see
 // window_a), so a code is a candidate iff its lower bound s_k - D_k reaches the best upper
 // bound min_j (s_j + D_j).
+#include <cstdlib>
+
 #include "host_common.h"
 #include "tc_gemm.cuh"
 
@@ -47,6 +49,7 @@ struct VqWorkspace {
   int* rr_list;       // [G * M][kRREntry] items whose window holds > 1 candidate (fp64 re-rank):
                       // {item, n (-1: scan the records), candidate codes ...}
   int* rr_count;      // [1]
+  int* row_tok;       // [M] source row -> token (-1: not a token row); run mode over pre-split rows
 };
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -69,6 +72,7 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
   size_t o_sc = take((size_t)G * M * nchunk * kVqCap * 4);
   size_t o_rl = take((size_t)G * M * kRREntry * 4);
   size_t o_rc = take(4);
+  size_t o_rt = take((size_t)M * 4);
   if (w && base) {
     uint8_t* b = reinterpret_cast<uint8_t*>(base);
     w->x_hi = reinterpret_cast<__nv_bfloat16*>(b + o_hi);
@@ -81,6 +85,7 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
     w->rec_score = reinterpret_cast<float*>(b + o_sc);
     w->rr_list = reinterpret_cast<int*>(b + o_rl);
     w->rr_count = reinterpret_cast<int*>(b + o_rc);
+    w->row_tok = reinterpret_cast<int*>(b + o_rt);
   }
   return off;
 }
@@ -150,7 +155,7 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
   const int warps = blockDim.x >> 5;
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  // the re-rank list is appended to by the run-mode GEMM epilogue that follows: reset here
+  // the re-rank list is appended to by the GEMM epilogue that follows: reset here
   if (blockIdx.x == 0 && threadIdx.x == 0) *w.rr_count = 0;
   if (r >= M) return;
   const int src = rows ? rows[r] : r;
@@ -181,6 +186,7 @@ __global__ void vq_split_v4_kernel(const float* __restrict__ x, int M, int ldx,
   const int warps = blockDim.x >> 5;
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
+  // the re-rank list is appended to by the GEMM epilogue that follows: reset here
   if (blockIdx.x == 0 && threadIdx.x == 0) *w.rr_count = 0;
   if (r >= M) return;
   const int src = rows ? rows[r] : r;
@@ -216,7 +222,30 @@ __global__ void vq_split_v4_kernel(const float* __restrict__ x, int M, int ldx,
   }
 }
 
+// Inverse of the token -> source-row map for the run-mode GEMM over pre-split stack rows
+// (two launches: every row to -1, then the token rows; also resets the re-rank count).
+__global__ void vq_row_tok_fill_kernel(int* row_tok, int R, int* rr_count) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == 0) *rr_count = 0;
+  if (r < R) row_tok[r] = -1;
+}
+__global__ void vq_row_tok_scatter_kernel(const int32_t* __restrict__ rows, int M, int* row_tok) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < M) row_tok[rows[m]] = m;
+}
+
 // ---------------------------------------------------------- epilogue
+__device__ __forceinline__ void vq_decide(const AstraCodebook& cb, const float* __restrict__ x,
+                                          int ldx, int src_row, int tok, int g, int Mtok,
+                                          size_t rec0, int nchunk, const VqWorkspace& w,
+                                          int32_t* __restrict__ idx_out, int32_t* __restrict__ stats,
+                                          bool inline_rr, int lane);
+
+// Records epilogue (G = 1 over all 148 SMs; a row's codes span several tiles on different CTA
+// pairs): per (row, 64-code part) the window's upper bound, min lower bound and up to kVqCap
+// candidates; vq_finalize_kernel merges them.  (Finalizing inside the GEMM — the CTA completing
+// a row block decides its rows — measured 141 us vs 52 + 7: the latency-bound decisions land
+// on a few CTAs' critical paths.)
 template <int BN>
 struct VqEpilogue {
   static constexpr bool kStateful = false;
@@ -298,6 +327,7 @@ struct VqEpilogue {
       w.rec_cnt[rec] = cnt;
     }
   }
+
 };
 
 // Grouped codebooks (G > 1): the GEMM runs in "runs" (TileSched::runs) — a CTA pair takes a
@@ -374,9 +404,11 @@ struct VqRunEpilogue {
   const float4* c_win;      // [G, K] {||c||^2, ||c||, eps ||c||^2, 0}
   const float* c_norm_max;  // [G] max ||c|| (rounded up)
   VqWorkspace w;
-  int32_t* idx_out;         // [M, G]
+  int32_t* idx_out;         // [Mtok, G]
   int32_t* stats;           // nullable: stats[2] += window candidates
   int G;
+  const int32_t* row_tok;   // nullable: GEMM row -> token (pre-split stack rows); else identity
+  int Mtok;
 
   // Before the tile's accumulator is ready: the window terms of this part's codes into smem
   // and, on a run's first tile, the row's window constants.
@@ -494,7 +526,8 @@ struct VqRunEpilogue {
     }
     const int quarter = row_in_tile >> 5;
     asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(32 * kEpiParts) : "memory");
-    if (part == 0 && ok) {
+    const int tok = !ok ? -1 : row_tok ? __ldg(row_tok + row) : row;
+    if (part == 0 && tok >= 0) {
       // stage areas of the warps of this quarter are kEpiStageBytes * 4 apart (warp + 4 p)
       float U = INFINITY;
 #pragma unroll
@@ -518,11 +551,11 @@ struct VqRunEpilogue {
       }
       if (stats) atomicAdd(&stats[2], n);
       if (n == 1 && !ovf) {
-        idx_out[(size_t)row * G + g] = only;
+        idx_out[(size_t)tok * G + g] = only;
       } else {
         const int slot = atomicAdd(w.rr_count, 1);
         int* ent = w.rr_list + (size_t)slot * kRREntry;
-        ent[0] = g * M + row;
+        ent[0] = g * Mtok + tok;
         if (!ovf && n >= 1 && n <= 8) {
           ent[1] = n;
 #pragma unroll
@@ -543,33 +576,43 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// sum_e a[e] b[e] over this lane's elements e = lane, lane + 32, ... in fp64 (the warp sum of
+// it is the dot product); loads batched 8 per lane so a 768-wide row costs 3 round trips, not 24
+__device__ __forceinline__ double lane_dot64(const float* a, const float* b, int gd, int lane) {
+  double acc = 0.0;
+  for (int base = 0; base < gd; base += 256) {
+    float av[8], bv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = base + lane + 32 * i;
+      av[i] = e < gd ? __ldg(a + e) : 0.0f;
+      bv[i] = e < gd ? __ldg(b + e) : 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (base + lane + 32 * i < gd) acc = fma((double)av[i], (double)bv[i], acc);
+  }
+  return acc;
+}
+
 // exact reference distance (vq.py:130 evaluation order): (pp - 2 pc) + cc, fp64
 __device__ __forceinline__ double exact_d2(const float* xr, const float* c, int gd, double pp,
                                            double cc, int lane) {
-  double pc = 0.0;
-  for (int e = lane; e < gd; e += 32) pc = fma((double)__ldg(xr + e), (double)__ldg(c + e), pc);
-  pc = warp_sum_d(pc);
+  const double pc = warp_sum_d(lane_dot64(xr, c, gd, lane));
   return (pp - 2.0 * pc) + cc;
 }
 
-// One warp per (g, row).  Lane c reads chunk record c (2*ceil(K/256) records per row); the
-// window test, survivor count and the single survivor come out of warp shuffles.  A single
-// survivor is the answer; several (or a chunk whose candidate list overflowed) are re-ranked
-// by the warp in exact fp64 with the reference's expression (||p||^2 - 2 p.c) + ||c||^2,
-// ties to the lowest index.
-__global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x, int M, int ldx,
-                                   const int32_t* __restrict__ rows, VqWorkspace w, int nchunk,
-                                   int32_t* __restrict__ idx_out, int32_t* __restrict__ stats,
-                                   int Mrec, int rec_by_row) {
-  const int warps = blockDim.x >> 5;
-  const int item = blockIdx.x * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+// Decide one (g, token) item from its chunk records (one warp; lane c reads record c): a single
+// window survivor is the answer.  Several go to the fp64 re-rank — inline (inline_rr: the warp
+// scores the <= kRRCands candidates itself with the reference expression, vq.py:130) or as an
+// entry of the re-rank list; an overflowed record list always goes to the list.
+__device__ __forceinline__ void vq_decide(const AstraCodebook& cb, const float* __restrict__ x,
+                                          int ldx, int src_row, int tok, int g, int Mtok,
+                                          size_t rec0, int nchunk, const VqWorkspace& w,
+                                          int32_t* __restrict__ idx_out, int32_t* __restrict__ stats,
+                                          bool inline_rr, int lane) {
   const int G = cb.groups;
-  if (item >= G * M) return;
-  const int g = item / M, row = item % M;
-  // records are indexed by token (gathered split) or by source row (pre-split stack)
-  const int rr = rec_by_row ? rows[row] : row;
-  const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
+  const int item = g * Mtok + tok, row = tok;
   // one round of independent loads: lane c holds chunk record c (nchunk <= 32 for K <= 2048;
   // larger codebooks loop)
   // U = min over chunks of U_chunk bounds the true best score from above; a chunk matters if
@@ -625,7 +668,34 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
     only = min(only, __shfl_xor_sync(0xffffffffu, only, o));
     overflow |= __shfl_xor_sync(0xffffffffu, overflow, o);
   }
-  if (overflow || n > 1) {
+  if (inline_rr && !overflow && n > 1 && n <= kRRCands) {
+    // several window candidates: the warp re-ranks them now, exact fp64 with the reference's
+    // expression (||p||^2 - 2 p.c) + ||c||^2, ties to the lowest index
+    const int gd = cb.group_dim, K = cb.size;
+    const float* xr = x + (size_t)src_row * ldx + (size_t)g * gd;
+    const float* cents = cb.centroids + (size_t)g * K * gd;
+    const double pp = warp_sum_d(lane_dot64(xr, xr, gd, lane));
+    double bd = INFINITY;
+    int bi = 0x7FFFFFFF;
+#pragma unroll
+    for (int i = 0; i < kVqCap; ++i) {
+      uint32_t m = __ballot_sync(0xffffffffu, (live >> i) & 1u);
+      while (m) {
+        const int srcl = __ffs(m) - 1;
+        m &= m - 1;
+        const int k = __shfl_sync(0xffffffffu, ix[i], srcl);
+        const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cb.c_sq64[(size_t)g * K + k], lane);
+        if (d < bd || (d == bd && k < bi)) {
+          bd = d;
+          bi = k;
+        }
+      }
+    }
+    if (lane == 0) {
+      idx_out[(size_t)row * G + g] = bi;
+      if (stats) atomicAdd(&stats[0], 1);
+    }
+  } else if (overflow || n > 1) {
     // several window candidates: exact fp64 re-rank by vq_rerank_kernel, handed the compacted
     // candidate list (codes in increasing order) when it fits
     int slot = 0;
@@ -653,6 +723,25 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
     idx_out[(size_t)row * G + g] = only;
   }
   if (lane == 0 && stats) atomicAdd(&stats[2], n);
+}
+
+__global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x, int M, int ldx,
+                                   const int32_t* __restrict__ rows, VqWorkspace w, int nchunk,
+                                   int32_t* __restrict__ idx_out, int32_t* __restrict__ stats,
+                                   int Mrec, int rec_by_row) {
+  const int warps = blockDim.x >> 5;
+  const int item = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const int G = cb.groups;
+  if (item >= G * M) return;
+  const int g = item / M, row = item % M;
+  // records are indexed by token (gathered split) or by source row (pre-split stack)
+  const int rr = rec_by_row ? rows[row] : row;
+  const size_t rec0 = ((size_t)g * Mrec + rr) * nchunk;
+  // (re-ranking the multi-candidate rows in place measured slower: 27.7 vs 7.4 + 10.2 us — the
+  // re-rank kernel's batched loads beat the per-row warps' dependent round trips)
+  vq_decide(cb, x, ldx, rows ? rows[row] : row, row, g, M, rec0, nchunk, w, idx_out, stats, false,
+            lane);
 }
 
 // Exact fp64 re-rank of the listed items (one warp per item, grid-stride over the list): the
@@ -1050,7 +1139,8 @@ static cudaError_t vq_launch_gemm(const AstraCodebook& cb, const CUtensorMap& ta
 template <int BN>
 static cudaError_t vq_launch_run(const AstraCodebook& cb, const CUtensorMap& ta,
                                  const CUtensorMap& talo, int M, VqWorkspace w, int32_t* idx_out,
-                                 int32_t* stats, int cluster, cudaStream_t s) {
+                                 int32_t* stats, int cluster, cudaStream_t s,
+                                 const int32_t* row_tok, int Mtok) {
   const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
   CUtensorMap tb, tblo;
   if (make_tmap_2d(&tb, cb.c_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * K, gdp, gdp,
@@ -1059,7 +1149,8 @@ static cudaError_t vq_launch_run(const AstraCodebook& cb, const CUtensorMap& ta,
                    BN / cluster, kBK, true))
     return cudaErrorInvalidValue;
   VqRunEpilogue<BN> epi{M, K, reinterpret_cast<const float4*>(cb.c_win),
-                         reinterpret_cast<const float*>(cb.c_norm_max), w, idx_out, stats, G};
+                         reinterpret_cast<const float*>(cb.c_norm_max), w, idx_out, stats, G,
+                         row_tok, Mtok};
   TileSched sched{(M + kBM - 1) / kBM, (K + BN - 1) / BN, G, 1};
   sched.runs = 1;
   return cluster == 2 ? launch_tc_gemm<BN, 3, 3, 2>(ta, talo, tb, tblo, gdp, sched, M, K, epi, s,
@@ -1076,7 +1167,7 @@ static cudaError_t vq_launch_run(const AstraCodebook& cb, const CUtensorMap& ta,
 static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const void* a_lo, int lda,
                             int Mg, VqWorkspace w, const float* x, int M, int ldx,
                             const int32_t* rows, int rec_by_row, int32_t* idx_out, int32_t* stats,
-                            cudaStream_t s) {
+                            cudaStream_t s, const int32_t* row_tok_in = nullptr) {
   const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
   if (Mg <= 0 || M <= 0) return ASTRA_OK;   // (the GEMM's tile (0, 0) resets the re-rank count)
   const int cluster = (Mg > kBM) ? 2 : 1;  // CTA pairs split the codebook tile (cta_group::2)
@@ -1091,12 +1182,29 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
   if ((st = make_tmap_2d(&talo, a_lo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)G * Mg, gdp,
                          lda, kBM, kBK, true)))
     return st;
-  if (G > 1 && !rec_by_row) {
+  // G = 1 over the pre-split stack: run mode only when it costs no extra waves (a run keeps a
+  // pair for ceil(K / 256) tiles; with fewer row blocks than pairs the idle SMs cost more than
+  // the finalize pass saves — ViT-B B=64: 50 blocks on 74 pairs, 58 us vs 51 + 9)
+  const long pairs = num_sms() / 2, rblocks = (Mg + 2 * kBM - 1) / (2 * kBM), ct = (K + kVqBN - 1) / kVqBN;
+  const bool run_g1 = rec_by_row && cluster == 2 && K >= kVqBN &&
+                      ((rblocks + pairs - 1) / pairs) * ct <= (rblocks * ct + pairs - 1) / pairs;
+  if (G > 1 || run_g1) {
+    // Run mode: grouped codebooks (token-gathered operands), and G = 1 over the pre-split stack
+    // (a CTA pair per 256-row block sweeps the whole codebook; rows decided in the epilogue —
+    // no records, no finalize pass; the re-rank takes the ~5% multi-candidate rows).
+    const int* row_tok = row_tok_in;
+    if (rec_by_row && !row_tok) {
+      vq_row_tok_fill_kernel<<<(Mg + 255) / 256, 256, 0, s>>>(w.row_tok, Mg, w.rr_count);
+      vq_row_tok_scatter_kernel<<<(M + 255) / 256, 256, 0, s>>>(rows, M, w.row_tok);
+      row_tok = w.row_tok;
+    } else if (rec_by_row) {   // the caller's map: only the re-rank list count to reset
+      vq_row_tok_fill_kernel<<<1, 32, 0, s>>>(w.row_tok, 0, w.rr_count);
+    }
     const long runs = (long)G * ((Mg + kBM * cluster - 1) / (kBM * cluster));
-    const int rbn = (K <= kVqBNMin || runs * cluster < num_sms()) ? kVqBNMin : kVqBN;
+    const int rbn = (K <= kVqBNMin || (G > 1 && runs * cluster < num_sms())) ? kVqBNMin : kVqBN;
     const cudaError_t er = rbn == kVqBN
-        ? vq_launch_run<kVqBN>(cb, ta, talo, Mg, w, idx_out, stats, cluster, s)
-        : vq_launch_run<kVqBNMin>(cb, ta, talo, Mg, w, idx_out, stats, cluster, s);
+        ? vq_launch_run<kVqBN>(cb, ta, talo, Mg, w, idx_out, stats, cluster, s, row_tok, M)
+        : vq_launch_run<kVqBNMin>(cb, ta, talo, Mg, w, idx_out, stats, cluster, s, row_tok, M);
     ASTRA_CUDA_CHECK(er);
     const int gd = cb.group_dim;
     if (gd <= 128 && gd % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0)
@@ -1150,11 +1258,12 @@ extern "C" int64_t astra_vq_encode_split_workspace(int R, int size) {
   return (int64_t)carve(nullptr, nullptr, R, 1, size, 0);
 }
 
-extern "C" int astra_vq_encode_split(const AstraCodebook* cbp, const float* x, int ldx,
-                                     const void* x_hi, const void* x_lo, int ld_split,
-                                     const float* x_norm, int R, const int32_t* rows, int M,
-                                     int32_t* idx_out, int32_t* stats, void* workspace,
-                                     int64_t workspace_bytes, void* stream) {
+extern "C" int astra_vq_encode_split_ex(const AstraCodebook* cbp, const float* x, int ldx,
+                                        const void* x_hi, const void* x_lo, int ld_split,
+                                        const float* x_norm, int R, const int32_t* rows, int M,
+                                        const int32_t* row_token, int32_t* idx_out,
+                                        int32_t* stats, void* workspace, int64_t workspace_bytes,
+                                        void* stream) {
   ASTRA_REQUIRE(cbp && x && x_hi && x_lo && x_norm && rows && idx_out, ASTRA_ERR_SHAPE,
                 "astra_vq_encode_split: null argument");
   const AstraCodebook cb = *cbp;
@@ -1171,7 +1280,16 @@ extern "C" int astra_vq_encode_split(const AstraCodebook* cbp, const float* x, i
   w.x_lo = nullptr;
   w.x_norm = const_cast<float*>(x_norm);
   return vq_gemm_finalize(cb, x_hi, x_lo, ld_split, R, w, x, M, ldx, rows, 1, idx_out, stats,
-                          as_stream(stream));
+                          as_stream(stream), row_token);
+}
+
+extern "C" int astra_vq_encode_split(const AstraCodebook* cbp, const float* x, int ldx,
+                                     const void* x_hi, const void* x_lo, int ld_split,
+                                     const float* x_norm, int R, const int32_t* rows, int M,
+                                     int32_t* idx_out, int32_t* stats, void* workspace,
+                                     int64_t workspace_bytes, void* stream) {
+  return astra_vq_encode_split_ex(cbp, x, ldx, x_hi, x_lo, ld_split, x_norm, R, rows, M, nullptr,
+                                  idx_out, stats, workspace, workspace_bytes, stream);
 }
 
 extern "C" int astra_vq_decode(const AstraCodebook* cbp, const int32_t* idx, int M, float* out,

@@ -305,7 +305,13 @@ class AstraRuntime:
         else:
             self.xs_hi = self.xs_lo = self.xnorm = None
             ws = cb0.workspace_bytes(max(self.n_content, 1)) if cb0 else 1
-        self.vq_ws = e(max(ws, 1), dt=torch.uint8)
+        # zero-filled once: the fused VQ finalize's tile counters and re-rank list count are
+        # self-cleaning after that (astra_vq_encode_split_ex)
+        self.vq_ws = torch.zeros(max(ws, 1), dtype=torch.uint8, device=dev)
+        # stack row -> token index (-1: replica rows), the inverse of content_rows
+        rt = np.full(R, -1, dtype=np.int32)
+        rt[self.content_rows.cpu().numpy()] = np.arange(self.n_content, dtype=np.int32)
+        self.row_token = torch.from_numpy(rt).to(dev)
         # sticky device-side error flags: [0] a received code >= K (unpack / packed key map),
         # [1] a decode index out of range; read once per forward by check_errors()
         self.err_flags = torch.zeros(2, dtype=torch.int32, device=dev)
@@ -474,11 +480,11 @@ class AstraRuntime:
         if encode:
             with self._op("vq_encode"):
                 if split:
-                    _native.call("astra_vq_encode_split", ctypes.byref(cb.struct),
+                    _native.call("astra_vq_encode_split_ex", ctypes.byref(cb.struct),
                                  self.X.data_ptr(), D, self.xs_hi.data_ptr(),
                                  self.xs_lo.data_ptr(), D, self.xnorm.data_ptr(), R,
                                  self.content_rows.data_ptr(), self.n_content,
-                                 self.idx_local.data_ptr(),
+                                 self.row_token.data_ptr(), self.idx_local.data_ptr(),
                                  self.vq_stats.data_ptr() if self.collect_vq_stats else None,
                                  self.vq_ws.data_ptr(), self.vq_ws.numel(), s)
                 else:
