@@ -57,6 +57,8 @@ __device__ __forceinline__ float ld_elem(const void* base, size_t off) {
 
 template <bool BF16, int kDH>
 __global__ void __launch_bounds__(256) attention_simt_kernel(AttnArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int kPad = kDH + 1;
   constexpr int kDPT = kDH / 4;   // output dims per thread
   extern __shared__ float smem_f[];
@@ -287,6 +289,7 @@ __device__ __forceinline__ uint32_t attn_vis32(const short* kpos, int col0, int 
 }
 
 __global__ void __launch_bounds__(kTcThreads, 2) attention_tc_kernel(AttnArgs a) {
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -340,6 +343,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) attention_tc_kernel(AttnArgs a)
   tc_fence_before();
   __syncthreads();   // TMEM address and barrier init visible to all
   tc_fence_after();
+  pdl_trigger();   // after the TMEM allocation (ptx.cuh)
   const uint32_t tmem = *tslot, tS = tmem, tO = tmem + 64;
   uint32_t phase = 0;
 
@@ -894,6 +898,7 @@ __device__ __forceinline__ void p_softmax(const AttnArgs& a, int qtiles, int pip
 template <bool kCausal>
 __global__ void __launch_bounds__(kPThreads, 1)
     attention_tcp_kernel(AttnArgs a, const __grid_constant__ PMaps mp, int qtiles) {
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -939,6 +944,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();   // after the TMEM allocation (ptx.cuh)
   const uint32_t tmem = *tslot;
 
   if (warp < 8) {
@@ -1053,6 +1059,7 @@ __device__ __forceinline__ void s_group_exp(const uint32_t (&rr)[32], uint32_t m
 template <bool kCausal>
 __global__ void __launch_bounds__(kSThreads, 1)
     attention_tcs_kernel(AttnArgs a, const __grid_constant__ PMaps mp, int qtiles) {
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -1107,6 +1114,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();   // after the TMEM allocation (ptx.cuh)
   const uint32_t tmem = *tslot;
   PIter it;
   it.step = 1;
@@ -1515,6 +1523,7 @@ __device__ __forceinline__ const float* t3_key_row(const AttnArgs& a, int src, b
 }
 
 __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a) {
+  pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                            ~uintptr_t(1023));
@@ -1577,6 +1586,7 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();   // after the TMEM allocation (ptx.cuh)
   const uint32_t tmem = *tslot, tS = tmem, tPl = tmem + 128, tO = tmem + 192;
   uint32_t phase = 0;
 
@@ -1767,9 +1777,9 @@ static int launch_attn(const AttnArgs& a, dim3 grid, cudaStream_t st) {
     configured = true;
   }
   if (a.in_bf16)
-    attention_simt_kernel<true, DH><<<grid, 256, smem, st>>>(a);
+    launch_k(attention_simt_kernel<true, DH>, grid, 256, smem, st, a);
   else
-    attention_simt_kernel<false, DH><<<grid, 256, smem, st>>>(a);
+    launch_k(attention_simt_kernel<false, DH>, grid, 256, smem, st, a);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
@@ -1845,17 +1855,17 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
         return rc;
       if (g_attention_variant == 2) {
         if (causal)
-          attention_tcs_kernel<true><<<grid, kSThreads, kSSmem, st>>>(a, mp, qtiles);
+          launch_kp(attention_tcs_kernel<true>, grid, kSThreads, kSSmem, st, a, mp, qtiles);
         else
-          attention_tcs_kernel<false><<<grid, kSThreads, kSSmem, st>>>(a, mp, qtiles);
+          launch_kp(attention_tcs_kernel<false>, grid, kSThreads, kSSmem, st, a, mp, qtiles);
       } else if (causal) {
-        attention_tcp_kernel<true><<<grid, kPThreads, kPSmem, st>>>(a, mp, qtiles);
+        launch_kp(attention_tcp_kernel<true>, grid, kPThreads, kPSmem, st, a, mp, qtiles);
       } else {
-        attention_tcp_kernel<false><<<grid, kPThreads, kPSmem, st>>>(a, mp, qtiles);
+        launch_kp(attention_tcp_kernel<false>, grid, kPThreads, kPSmem, st, a, mp, qtiles);
       }
     } else {
       dim3 tgrid(num_segs, heads, qtiles);
-      attention_tc_kernel<<<tgrid, kTcThreads, kTcSmem, st>>>(a);
+      launch_kp(attention_tc_kernel, tgrid, kTcThreads, kTcSmem, st, a);
     }
     ASTRA_CUDA_CHECK(cudaGetLastError());
     return ASTRA_OK;
@@ -1878,7 +1888,7 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
       configured3 = true;
     }
     dim3 tgrid(num_segs, heads, (max_nq + kT3Q - 1) / kT3Q);
-    attention_tc3_kernel<<<tgrid, kT3Threads, kT3Smem, st>>>(a);
+    launch_kp(attention_tc3_kernel, tgrid, kT3Threads, kT3Smem, st, a);
     ASTRA_CUDA_CHECK(cudaGetLastError());
     return ASTRA_OK;
   }

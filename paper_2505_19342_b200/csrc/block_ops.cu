@@ -32,6 +32,8 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
                                  int ld_bf, __nv_bfloat16* __restrict__ xs_hi,
                                  __nv_bfloat16* __restrict__ xs_lo, int ld_xs,
                                  float* __restrict__ x_norm, LnGather gat = LnGather{}) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   // one row per warp, every row of the grid in flight at once (no grid-stride tail: the
@@ -118,6 +120,8 @@ __global__ void layernorm_generic_kernel(const float* __restrict__ x, int M, int
                                          float* __restrict__ out_f32, int ld_f32,
                                          __nv_bfloat16* __restrict__ out_hi,
                                          __nv_bfloat16* __restrict__ out_lo, int ld_bf) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int row = blockIdx.x * warps + (threadIdx.x >> 5); row < M; row += gridDim.x * warps) {
@@ -153,6 +157,8 @@ __global__ void embed_stack_kernel(const float* __restrict__ x, const float* __r
                                    const float* __restrict__ cls, const int32_t* __restrict__ row_src,
                                    const int32_t* __restrict__ row_pos, int rows, int D,
                                    float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
@@ -182,6 +188,8 @@ __global__ void embed_stack_kernel(const float* __restrict__ x, const float* __r
 // reps: [N, B, D] in device order -> out [B, D] = (((r0 + r1) + r2) + ...) / N
 __global__ void replica_mean_kernel(const float* __restrict__ reps, int N, int BD,
                                     float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= BD) return;
   float s = reps[i];
@@ -193,6 +201,8 @@ __global__ void replica_mean_kernel(const float* __restrict__ reps, int N, int B
 __global__ void gather_rows_kernel(const float* __restrict__ src, int lds,
                                    const int32_t* __restrict__ idx, int rows, int D,
                                    float* __restrict__ out, int ldo) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
@@ -213,6 +223,8 @@ __global__ void gather_rows_kernel(const float* __restrict__ src, int lds,
 //                   (G = 1: the K/V table row of its code)  or  -(t+1) when codes == NULL
 __global__ void key_map_kernel(const int32_t* __restrict__ key_map, int n,
                                const int32_t* __restrict__ codes, int32_t* __restrict__ key_src) {
+  pdl_wait();
+  pdl_trigger();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int m = key_map[j];
@@ -237,6 +249,8 @@ __global__ void gather_kv_kernel(const int32_t* __restrict__ key_src, int n, int
                                  const uint8_t* __restrict__ k_remote,
                                  const uint8_t* __restrict__ v_remote, int ld_remote,
                                  int row_bytes, uint8_t* __restrict__ cache, int ld_cache) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < n; i += gridDim.x * warps) {
@@ -260,6 +274,8 @@ __global__ void append_kv_kernel(const uint8_t* __restrict__ k_new, const uint8_
                                  int ld_new, int rows, const int32_t* __restrict__ pos,
                                  int ld_blocks, int row_bytes, uint8_t* __restrict__ cache,
                                  int ld_cache) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= rows) return;
@@ -282,6 +298,8 @@ __global__ void argmax_rows_kernel(const float* __restrict__ logits, int cols, i
                                    int32_t* __restrict__ out, int out_stride,
                                    const int32_t* __restrict__ step_pos, int pos_base,
                                    int32_t* __restrict__ next_tok) {
+  pdl_wait();
+  pdl_trigger();
   const int row = blockIdx.x;
   const float* lr = logits + (size_t)row * ld;
   float bv = -INFINITY;
@@ -325,6 +343,8 @@ __global__ void argmax_rows_kernel(const float* __restrict__ logits, int cols, i
 // one decode step done: every image's position and key count advance by one
 __global__ void decode_advance_kernel(int32_t* __restrict__ pos, int32_t* __restrict__ segs,
                                       int rows) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= rows) return;
   pos[b] += 1;
@@ -351,6 +371,8 @@ __global__ void segment_mean_f64_kernel(const double* __restrict__ pts, int ld,
                                         const int32_t* __restrict__ order,
                                         const int32_t* __restrict__ seg, int k, int dim,
                                         double* __restrict__ mean, double* __restrict__ sums) {
+  pdl_wait();
+  pdl_trigger();
   const int d = blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (d >= dim || c >= k) return;
@@ -369,6 +391,8 @@ __global__ void embed_tokens_kernel(const float* __restrict__ emb, const float* 
                                     const int32_t* __restrict__ row_src,
                                     const int32_t* __restrict__ row_pos, int rows, int D,
                                     float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < rows; r += gridDim.x * warps) {
@@ -408,18 +432,18 @@ extern "C" int astra_layernorm_ex(const float* x, int M, int D, int ldx, const f
   const int grid = grid_rows(M, 8);
   const int grid1 = (M + 3) / 4;   // vector kernels: one row per warp, 4 warps per block
   if (vec && D == 768)
-    layernorm_kernel<6><<<grid1, 128, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
-                                             ld_bf, xh, xl, ld_xs, x_norm);
+    launch_k(layernorm_kernel<6>, grid1, 128, 0, s, x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+                                             ld_bf, xh, xl, ld_xs, x_norm, LnGather{});
   else if (vec && D == 1024)
-    layernorm_kernel<8><<<grid1, 128, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
-                                             ld_bf, xh, xl, ld_xs, x_norm);
+    launch_k(layernorm_kernel<8>, grid1, 128, 0, s, x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+                                             ld_bf, xh, xl, ld_xs, x_norm, LnGather{});
   else if (vec && D == 512)
-    layernorm_kernel<4><<<grid1, 128, 0, s>>>(x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
-                                             ld_bf, xh, xl, ld_xs, x_norm);
+    launch_k(layernorm_kernel<4>, grid1, 128, 0, s, x, M, ldx, gain, bias, eps, out_f32, ld_f32, hi, lo,
+                                             ld_bf, xh, xl, ld_xs, x_norm, LnGather{});
   else {
     ASTRA_REQUIRE(xs_hi == nullptr && x_norm == nullptr, ASTRA_ERR_SHAPE,
                   "layernorm: split / norm outputs need D in {512, 768, 1024}");
-    layernorm_generic_kernel<<<grid, 256, 0, s>>>(x, M, D, ldx, gain, bias, eps, out_f32, ld_f32,
+    launch_k(layernorm_generic_kernel, grid, 256, 0, s, x, M, D, ldx, gain, bias, eps, out_f32, ld_f32,
                                                   hi, lo, ld_bf);
   }
   ASTRA_CUDA_CHECK(cudaGetLastError());
@@ -446,13 +470,13 @@ extern "C" int astra_vq_decode_layernorm(const AstraCodebook* cbp, const int32_t
   const LnGather gat{cb.centroids, idx, cb.groups, cb.size, cb.group_dim, err_flag};
   const int grid1 = (M + 3) / 4;
   if (D == 768)
-    layernorm_kernel<6><<<grid1, 128, 0, s>>>(nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
+    launch_k(layernorm_kernel<6>, grid1, 128, 0, s, nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
                                              ld_bf, nullptr, nullptr, 0, nullptr, gat);
   else if (D == 1024)
-    layernorm_kernel<8><<<grid1, 128, 0, s>>>(nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
+    launch_k(layernorm_kernel<8>, grid1, 128, 0, s, nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
                                              ld_bf, nullptr, nullptr, 0, nullptr, gat);
   else
-    layernorm_kernel<4><<<grid1, 128, 0, s>>>(nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
+    launch_k(layernorm_kernel<4>, grid1, 128, 0, s, nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,
                                              ld_bf, nullptr, nullptr, 0, nullptr, gat);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -470,7 +494,7 @@ extern "C" int astra_embed_stack(const float* x, const float* pos, const float* 
                                  float* out, void* stream) {
   ASTRA_REQUIRE(D >= 1, ASTRA_ERR_SHAPE, "embed: bad width");
   if (rows == 0) return ASTRA_OK;
-  embed_stack_kernel<<<grid_rows(rows, 8), 256, 0, as_stream(stream)>>>(x, pos, cls, row_src,
+  launch_k(embed_stack_kernel, grid_rows(rows, 8), 256, 0, as_stream(stream), x, pos, cls, row_src,
                                                                        row_pos, rows, D, out);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -481,7 +505,7 @@ extern "C" int astra_replica_mean(const float* reps, int N, int B, int D, float*
   ASTRA_REQUIRE(N >= 1, ASTRA_ERR_SHAPE, "no class-token replicas to aggregate");
   const int bd = B * D;
   if (bd == 0) return ASTRA_OK;
-  replica_mean_kernel<<<(bd + 255) / 256, 256, 0, as_stream(stream)>>>(reps, N, bd, out);
+  launch_k(replica_mean_kernel, (bd + 255) / 256, 256, 0, as_stream(stream), reps, N, bd, out);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
@@ -490,7 +514,7 @@ extern "C" int astra_gather_rows(const float* src, int lds, const int32_t* idx, 
                                  float* out, int ldo, void* stream) {
   ASTRA_REQUIRE(D >= 1 && lds >= D && ldo >= D, ASTRA_ERR_SHAPE, "gather_rows: bad widths");
   if (rows == 0) return ASTRA_OK;
-  gather_rows_kernel<<<grid_rows(rows, 8), 256, 0, as_stream(stream)>>>(src, lds, idx, rows, D,
+  launch_k(gather_rows_kernel, grid_rows(rows, 8), 256, 0, as_stream(stream), src, lds, idx, rows, D,
                                                                        out, ldo);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -503,6 +527,8 @@ __global__ void key_map_packed_kernel(const int32_t* __restrict__ key_map, int n
                                       const uint32_t* __restrict__ words, int wmax, int bits, int K,
                                       const int32_t* __restrict__ gofs, int nsend,
                                       int32_t* __restrict__ key_src, int32_t* err) {
+  pdl_wait();
+  pdl_trigger();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int m = key_map[j];
@@ -531,7 +557,7 @@ extern "C" int astra_key_map_packed(const int32_t* key_map, int n, const uint32_
                                     int32_t* key_src, int32_t* err_flag, void* stream) {
   ASTRA_REQUIRE(bits >= 1 && bits <= 31 && nsend >= 1, ASTRA_ERR_SHAPE, "key_map_packed: bad shape");
   if (n == 0) return ASTRA_OK;
-  key_map_packed_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(
+  launch_k(key_map_packed_kernel, (n + 255) / 256, 256, 0, as_stream(stream), 
       key_map, n, words, wmax, bits, size, gofs, nsend, key_src, err_flag);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -540,7 +566,7 @@ extern "C" int astra_key_map_packed(const int32_t* key_map, int n, const uint32_
 extern "C" int astra_key_map(const int32_t* key_map, int n, const int32_t* codes,
                              int32_t* key_src, void* stream) {
   if (n == 0) return ASTRA_OK;
-  key_map_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(key_map, n, codes, key_src);
+  launch_k(key_map_kernel, (n + 255) / 256, 256, 0, as_stream(stream), key_map, n, codes, key_src);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
@@ -551,7 +577,7 @@ extern "C" int astra_gather_kv(const int32_t* key_src, int n, int n_per, int ld_
                                int row_bytes, void* cache, int ld_cache_bytes, void* stream) {
   ASTRA_REQUIRE(row_bytes % 16 == 0 && n_per > 0, ASTRA_ERR_SHAPE, "gather_kv: bad row size");
   if (n == 0) return ASTRA_OK;
-  gather_kv_kernel<<<grid_rows(n, 8), 256, 0, as_stream(stream)>>>(
+  launch_k(gather_kv_kernel, grid_rows(n, 8), 256, 0, as_stream(stream), 
       key_src, n, n_per, ld_blocks, (const uint8_t*)k_local, (const uint8_t*)v_local,
       ld_local_bytes, (const uint8_t*)k_remote, (const uint8_t*)v_remote, ld_remote_bytes,
       row_bytes, (uint8_t*)cache, ld_cache_bytes);
@@ -564,7 +590,7 @@ extern "C" int astra_append_kv(const void* k_new, const void* v_new, int ld_new_
                                int ld_cache_bytes, void* stream) {
   ASTRA_REQUIRE(row_bytes % 16 == 0, ASTRA_ERR_SHAPE, "append_kv: bad row size");
   if (rows == 0) return ASTRA_OK;
-  append_kv_kernel<<<(rows + 7) / 8, 256, 0, as_stream(stream)>>>(
+  launch_k(append_kv_kernel, (rows + 7) / 8, 256, 0, as_stream(stream), 
       (const uint8_t*)k_new, (const uint8_t*)v_new, ld_new_bytes, rows, pos, ld_blocks, row_bytes,
       (uint8_t*)cache, ld_cache_bytes);
   ASTRA_CUDA_CHECK(cudaGetLastError());
@@ -575,7 +601,7 @@ extern "C" int astra_argmax_rows(const float* logits, int rows, int cols, int ld
                                  int out_stride, const int32_t* step_pos, int pos_base,
                                  int32_t* next_tok, void* stream) {
   if (rows == 0) return ASTRA_OK;
-  argmax_rows_kernel<<<rows, 1024, 0, as_stream(stream)>>>(logits, cols, ld, out, out_stride,
+  launch_k(argmax_rows_kernel, rows, 1024, 0, as_stream(stream), logits, cols, ld, out, out_stride,
                                                             step_pos, pos_base, next_tok);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -583,7 +609,7 @@ extern "C" int astra_argmax_rows(const float* logits, int rows, int cols, int ld
 
 extern "C" int astra_decode_advance(int32_t* pos, int32_t* segs, int rows, void* stream) {
   if (rows == 0) return ASTRA_OK;
-  decode_advance_kernel<<<(rows + 127) / 128, 128, 0, as_stream(stream)>>>(pos, segs, rows);
+  launch_k(decode_advance_kernel, (rows + 127) / 128, 128, 0, as_stream(stream), pos, segs, rows);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
@@ -594,7 +620,7 @@ extern "C" int astra_segment_mean_f64(const double* pts, int ld, const int32_t* 
   ASTRA_REQUIRE(k >= 0 && dim >= 0 && ld >= dim, ASTRA_ERR_SHAPE, "segment_mean: bad shape");
   if (k == 0 || dim == 0) return ASTRA_OK;
   dim3 grid((dim + 127) / 128, k);
-  segment_mean_f64_kernel<<<grid, 128, 0, as_stream(stream)>>>(pts, ld, order, seg, k, dim, mean,
+  launch_k(segment_mean_f64_kernel, grid, 128, 0, as_stream(stream), pts, ld, order, seg, k, dim, mean,
                                                               sums);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -605,7 +631,7 @@ extern "C" int astra_embed_tokens(const float* emb, const float* pos, const int3
                                   float* out, void* stream) {
   ASTRA_REQUIRE(rows >= 0 && D >= 1, ASTRA_ERR_SHAPE, "embed_tokens: bad shape");
   if (rows == 0) return ASTRA_OK;
-  embed_tokens_kernel<<<grid_rows(rows, 8), 256, 0, as_stream(stream)>>>(emb, pos, ids, row_src,
+  launch_k(embed_tokens_kernel, grid_rows(rows, 8), 256, 0, as_stream(stream), emb, pos, ids, row_src,
                                                                         row_pos, rows, D, out);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;

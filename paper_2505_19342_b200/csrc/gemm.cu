@@ -336,6 +336,8 @@ __global__ void gemm_simt_kernel(const __nv_bfloat16* __restrict__ a_hi,
                                  float* __restrict__ out_f32, int ld_f32,
                                  __nv_bfloat16* __restrict__ out_hi,
                                  __nv_bfloat16* __restrict__ out_lo, int ld_bf, int gelu) {
+  pdl_wait();
+  pdl_trigger();
   const int n = blockIdx.x * blockDim.x + threadIdx.x, m = blockIdx.y;
   if (n >= N || m >= M) return;
   const __nv_bfloat16* ah = a_hi + (size_t)m * lda;
@@ -383,7 +385,7 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                         (passes == 1 || (al16(a_lo) && al16(b_lo)));
     if (!tma_ok) {
       dim3 grid((N + 127) / 128, M);
-      gemm_simt_kernel<<<grid, 128, 0, as_stream(stream)>>>(
+      launch_k(gemm_simt_kernel, grid, 128, 0, as_stream(stream), 
           reinterpret_cast<const __nv_bfloat16*>(a_hi),
           passes == 3 ? reinterpret_cast<const __nv_bfloat16*>(a_lo) : nullptr, lda,
           reinterpret_cast<const __nv_bfloat16*>(b_hi),

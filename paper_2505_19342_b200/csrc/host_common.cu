@@ -1,4 +1,5 @@
 #include <cstdarg>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "host_common.h"
@@ -12,6 +13,14 @@ void set_last_error(const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
   va_end(ap);
+}
+
+int pdl_mode() {
+  static const int mode = [] {
+    const char* e = getenv("ASTRA_PDL");
+    return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
+  }();
+  return mode;
 }
 
 int num_sms() {

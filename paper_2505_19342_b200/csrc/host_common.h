@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <utility>
 
 #include "../../include/astra_b200.h"
 
@@ -41,5 +42,42 @@ int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, 
                  bool swizzle128);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Programmatic dependent launch: ASTRA_PDL=0 off, 1 every kernel, 2 (default) only the
+// persistent tensor-core kernels (GEMM, attention) — see DESIGN §3.5.
+int pdl_mode();
+inline bool pdl_enabled() { return pdl_mode() == 1; }
+inline bool pdl_persistent() { return pdl_mode() >= 1; }
+
+// Kernel launch with programmatic stream serialisation (see ptx.cuh pdl_wait): the kernel's
+// CTAs may launch while the stream's previous kernel drains and run their prologue (barrier
+// init, TMEM allocation, descriptor prefetch) before pdl_wait().  Errors surface through
+// cudaGetLastError() like a <<<>>> launch.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  return launch_pdl(pdl_enabled(), kern, grid, block, smem, s, std::forward<Args>(args)...);
+}
+// persistent tensor-core kernels (attention)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kp(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t s, Args&&... args) {
+  return launch_pdl(pdl_persistent(), kern, grid, block, smem, s, std::forward<Args>(args)...);
+}
 
 }  // namespace astra

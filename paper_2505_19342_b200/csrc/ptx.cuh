@@ -30,6 +30,17 @@ ASTRA_DEVICE bool elect_one() {
   return pred != 0;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Every kernel of the library is launched with programmatic stream serialisation (host
+// launch_k / launch_tc_gemm): its CTAs may start while the previous kernel of the stream is
+// still draining.  pdl_wait() blocks until that kernel has completed and its writes are
+// visible (a no-op without the attribute), so it precedes every global-memory access;
+// pdl_trigger() lets the next kernel's CTAs start their prologue.  Kernels that allocate TMEM
+// trigger only after their allocation: a dependent CTA that allocated first on the same SM
+// would otherwise hold the columns while waiting on this kernel (deadlock).
+ASTRA_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+ASTRA_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier
 ASTRA_DEVICE void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

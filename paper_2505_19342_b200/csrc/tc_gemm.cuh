@@ -195,6 +195,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL (ptx.cuh): barriers, TMEM and descriptors were set up while the previous kernel of the
+  // stream drained; every operand / epilogue access follows the wait
+  pdl_wait();
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -394,11 +398,13 @@ inline cudaError_t launch_tc_gemm(const CUtensorMap& ta, const CUtensorMap& talo
   cfg.blockDim = dim3(kGemmThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CLUSTER;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   // Persistent grid = the clusters that can be co-resident.  Clusters live inside one GPC, so
@@ -414,6 +420,7 @@ inline cudaError_t launch_tc_gemm(const CUtensorMap& ta, const CUtensorMap& talo
       fprintf(stderr, "tc_gemm<BN=%d,P=%d,C=%d>: %d co-resident clusters (%d SMs)\n", BN, PASSES,
               CLUSTER, n, sms);
   }
+  cfg.numAttrs = pdl_persistent() ? 2 : 1;
   const long max_units = max_clusters;
   const long work = sched.runs ? units_m * sched.num_b : total;   // runs: one unit per row block
   const int grid = (int)((work < max_units ? work : max_units) * CLUSTER);

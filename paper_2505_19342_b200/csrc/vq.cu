@@ -102,6 +102,8 @@ __device__ __forceinline__ float window_a(float xn) { return (2.0f * kTau + 2.0f
 
 // ------------------------------------------------------------ prepare
 __global__ void vq_prepare_kernel(AstraCodebook cb) {
+  pdl_wait();
+  pdl_trigger();
   // one warp per (g, k) code row
   const int warps = (blockDim.x >> 5);
   const int code = blockIdx.x * warps + (threadIdx.x >> 5);
@@ -131,6 +133,8 @@ __global__ void vq_prepare_kernel(AstraCodebook cb) {
 }
 
 __global__ void vq_normmax_kernel(AstraCodebook cb) {
+  pdl_wait();
+  pdl_trigger();
   const int g = blockIdx.x;
   float m = 0.f;
   for (int k = threadIdx.x; k < cb.size; k += blockDim.x)
@@ -152,6 +156,8 @@ __global__ void vq_normmax_kernel(AstraCodebook cb) {
 __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
                                 const int32_t* __restrict__ rows, int G, int gd, int gdp,
                                 VqWorkspace w) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -183,6 +189,8 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
 // in per / 32 steps.
 __global__ void vq_split_v4_kernel(const float* __restrict__ x, int M, int ldx,
                                    const int32_t* __restrict__ rows, int G, int gd, VqWorkspace w) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -225,11 +233,15 @@ __global__ void vq_split_v4_kernel(const float* __restrict__ x, int M, int ldx,
 // Inverse of the token -> source-row map for the run-mode GEMM over pre-split stack rows
 // (two launches: every row to -1, then the token rows; also resets the re-rank count).
 __global__ void vq_row_tok_fill_kernel(int* row_tok, int R, int* rr_count) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r == 0) *rr_count = 0;
   if (r < R) row_tok[r] = -1;
 }
 __global__ void vq_row_tok_scatter_kernel(const int32_t* __restrict__ rows, int M, int* row_tok) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m < M) row_tok[rows[m]] = m;
 }
@@ -729,6 +741,8 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
                                    const int32_t* __restrict__ rows, VqWorkspace w, int nchunk,
                                    int32_t* __restrict__ idx_out, int32_t* __restrict__ stats,
                                    int Mrec, int rec_by_row) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int item = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -758,6 +772,8 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
                                                         int32_t* __restrict__ idx_out,
                                                         int32_t* __restrict__ stats, int Mrec,
                                                         int rec_by_row, int part_codes) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_cand[8][32 * kVqCap];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int G = cb.groups, K = cb.size, gd = cb.group_dim;
@@ -1030,6 +1046,8 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
 // out[m, g*gd + e] = centroids[g][idx[m, g]][e]; one warp per (m, g), float4 when aligned.
 __global__ void vq_decode_kernel(AstraCodebook cb, const int32_t* __restrict__ idx, int M,
                                  float* __restrict__ out, int ldo, int32_t* err) {
+  pdl_wait();
+  pdl_trigger();
   const int warps = blockDim.x >> 5;
   const int item = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -1055,6 +1073,8 @@ __global__ void vq_decode_kernel(AstraCodebook cb, const int32_t* __restrict__ i
 // ------------------------------------------------------------ packing
 __global__ void pack_kernel(const int32_t* __restrict__ idx, int count, int bits,
                             uint32_t* __restrict__ words, int nwords) {
+  pdl_wait();
+  pdl_trigger();
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nwords) return;
   const long long b0 = (long long)w * 32, b1 = b0 + 32;
@@ -1072,6 +1092,8 @@ __global__ void pack_kernel(const int32_t* __restrict__ idx, int count, int bits
 
 __global__ void unpack_kernel(const uint32_t* __restrict__ words, int count, int bits, int K,
                               int32_t* __restrict__ idx, int32_t* err) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   uint32_t v = 0;
@@ -1102,8 +1124,8 @@ extern "C" int astra_vq_prepare(const AstraCodebook* cbp, void* stream) {
                 "padded_dim must be a multiple of 64 >= group_dim");
   cudaStream_t s = as_stream(stream);
   const int rows = cb.groups * cb.size;
-  vq_prepare_kernel<<<(rows + 7) / 8, 256, 0, s>>>(cb);
-  vq_normmax_kernel<<<cb.groups, 256, 0, s>>>(cb);
+  launch_k(vq_prepare_kernel, (rows + 7) / 8, 256, 0, s, cb);
+  launch_k(vq_normmax_kernel, cb.groups, 256, 0, s, cb);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
@@ -1194,11 +1216,11 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
     // no records, no finalize pass; the re-rank takes the ~5% multi-candidate rows).
     const int* row_tok = row_tok_in;
     if (rec_by_row && !row_tok) {
-      vq_row_tok_fill_kernel<<<(Mg + 255) / 256, 256, 0, s>>>(w.row_tok, Mg, w.rr_count);
-      vq_row_tok_scatter_kernel<<<(M + 255) / 256, 256, 0, s>>>(rows, M, w.row_tok);
+      launch_k(vq_row_tok_fill_kernel, (Mg + 255) / 256, 256, 0, s, w.row_tok, Mg, w.rr_count);
+      launch_k(vq_row_tok_scatter_kernel, (M + 255) / 256, 256, 0, s, rows, M, w.row_tok);
       row_tok = w.row_tok;
     } else if (rec_by_row) {   // the caller's map: only the re-rank list count to reset
-      vq_row_tok_fill_kernel<<<1, 32, 0, s>>>(w.row_tok, 0, w.rr_count);
+      launch_k(vq_row_tok_fill_kernel, 1, 32, 0, s, w.row_tok, 0, w.rr_count);
     }
     const long runs = (long)G * ((Mg + kBM * cluster - 1) / (kBM * cluster));
     const int rbn = (K <= kVqBNMin || (G > 1 && runs * cluster < num_sms())) ? kVqBNMin : kVqBN;
@@ -1208,10 +1230,10 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
     ASTRA_CUDA_CHECK(er);
     const int gd = cb.group_dim;
     if (gd <= 128 && gd % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0)
-      vq_rerank_kernel<true><<<num_sms() * 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
+      launch_k(vq_rerank_kernel<true>, num_sms() * 8, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                            stats, Mg, rec_by_row, bn / kEpiParts);
     else
-      vq_rerank_kernel<false><<<num_sms() * 4, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
+      launch_k(vq_rerank_kernel<false>, num_sms() * 4, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                             stats, Mg, rec_by_row, bn / kEpiParts);
     ASTRA_CUDA_CHECK(cudaGetLastError());
     return ASTRA_OK;
@@ -1220,10 +1242,10 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
                                     : vq_launch_gemm<kVqBNMin>(cb, ta, talo, Mg, w, nchunk, cluster, s);
   ASTRA_CUDA_CHECK(e);
   const int items = G * M;
-  vq_finalize_kernel<<<(items + 7) / 8, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out,
+  launch_k(vq_finalize_kernel, (items + 7) / 8, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                       stats, Mg, rec_by_row);
   ASTRA_CUDA_CHECK(cudaGetLastError());
-  vq_rerank_kernel<false><<<num_sms() * 4, 256, 0, s>>>(cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
+  launch_k(vq_rerank_kernel<false>, num_sms() * 4, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
                                                  Mg, rec_by_row, bn / kEpiParts);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
@@ -1247,9 +1269,9 @@ extern "C" int astra_vq_encode(const AstraCodebook* cbp, const float* x, int M, 
   const int gd = cb.group_dim, per = gd / 4;
   if (gd == gdp && gd % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
       (per <= 32 ? 32 % per == 0 : per % 32 == 0))
-    vq_split_v4_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, M, ldx, rows, G, gd, w);
+    launch_k(vq_split_v4_kernel, (M + 7) / 8, 256, 0, s, x, M, ldx, rows, G, gd, w);
   else
-    vq_split_kernel<<<(M + 7) / 8, 256, 0, s>>>(x, M, ldx, rows, G, gd, gdp, w);
+    launch_k(vq_split_kernel, (M + 7) / 8, 256, 0, s, x, M, ldx, rows, G, gd, gdp, w);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return vq_gemm_finalize(cb, w.x_hi, w.x_lo, gdp, M, w, x, M, ldx, rows, 0, idx_out, stats, s);
 }
@@ -1299,7 +1321,7 @@ extern "C" int astra_vq_decode(const AstraCodebook* cbp, const int32_t* idx, int
   ASTRA_REQUIRE(ldo >= cb.groups * cb.group_dim, ASTRA_ERR_SHAPE, "astra_vq_decode: ldo too small");
   if (M == 0) return ASTRA_OK;
   const int items = M * cb.groups;
-  vq_decode_kernel<<<(items + 7) / 8, 256, 0, as_stream(stream)>>>(cb, idx, M, out, ldo, err_flag);
+  launch_k(vq_decode_kernel, (items + 7) / 8, 256, 0, as_stream(stream), cb, idx, M, out, ldo, err_flag);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
@@ -1309,7 +1331,7 @@ extern "C" int astra_pack_indices(const int32_t* idx, int count, int bits, uint3
   ASTRA_REQUIRE(bits >= 0 && bits <= 31, ASTRA_ERR_SHAPE, "pack: bits out of range");
   const int nwords = (int)(((long long)count * bits + 31) / 32);
   if (nwords == 0) return ASTRA_OK;
-  pack_kernel<<<(nwords + 255) / 256, 256, 0, as_stream(stream)>>>(idx, count, bits, words, nwords);
+  launch_k(pack_kernel, (nwords + 255) / 256, 256, 0, as_stream(stream), idx, count, bits, words, nwords);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
@@ -1318,7 +1340,7 @@ extern "C" int astra_unpack_indices(const uint32_t* words, int count, int bits, 
                                     int32_t* idx, int32_t* err_flag, void* stream) {
   ASTRA_REQUIRE(bits >= 0 && bits <= 31, ASTRA_ERR_SHAPE, "unpack: bits out of range");
   if (count == 0) return ASTRA_OK;
-  unpack_kernel<<<(count + 255) / 256, 256, 0, as_stream(stream)>>>(words, count, bits, size, idx,
+  launch_k(unpack_kernel, (count + 255) / 256, 256, 0, as_stream(stream), words, count, bits, size, idx,
                                                                     err_flag);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
