@@ -719,9 +719,13 @@ __device__ __forceinline__ void p_mma(const AttnArgs& a, int qtiles, int pipe, c
     mbar_wait_spin(&b->p_full, ph);
     mbar_wait_spin(&b->v_full, ph);
     tc_fence_after();
+    // P V into two accumulators (even / odd 16-key steps, summed at read-back): the N=64 TS
+    // UMMAs are issue-bound when each depends on the previous one's accumulator
+    // (scripts/probes/pv_probe.cu: 13 steps 3018 -> 2304 cycles).  O_a / O_b sit on S columns
+    // 128..255, all read by the softmax before it published P.
     for (int kk = 0; kk < (ncols >> 4); ++kk)
-      umma_f16_ts(tS + 128, tS + kk * 8, sdesc_mnmajor_sw128(v_s + kk * 2048, 8192),
-                  idesc_bf16_f32_bmn(128, 64), kk > 0 ? 1u : 0u);
+      umma_f16_ts(tS + 128 + (kk & 1) * 64, tS + kk * 8, sdesc_mnmajor_sw128(v_s + kk * 2048, 8192),
+                  idesc_bf16_f32_bmn(128, 64), kk > 1 ? 1u : 0u);
     umma_commit(&b->o_full);
     umma_commit(&b->v_empty);
     p_trace(trace, 2 + pipe * 8, n);
@@ -845,14 +849,18 @@ __device__ __forceinline__ void p_softmax(const AttnArgs& a, int qtiles, int pip
     mbar_wait_spin(&b->o_full, ph);
     tc_fence_after();
     if (warp_rows) {
+      const bool two = valid > 16;   // O_b holds the odd 16-key steps (p_mma)
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t r0[32];
-        tmem_ld32(tS + 128 + lane_off + hh * 32, r0);
+      for (int hh = 0; hh < 4; ++hh) {
+        uint32_t r0[16], r1[16];
+        tmem_ld16(tS + 128 + lane_off + hh * 16, r0);
+        if (two) tmem_ld16(tS + 192 + lane_off + hh * 16, r1);
         tmem_ld_wait();
         // corr = 0 on an item's first chunk clears what the previous item left in o
 #pragma unroll
-        for (int d = 0; d < 32; ++d) o[hh * 32 + d] = fmaf(o[hh * 32 + d], corr, __uint_as_float(r0[d]));
+        for (int d = 0; d < 16; ++d)
+          o[hh * 16 + d] = fmaf(o[hh * 16 + d], corr,
+                                two ? __uint_as_float(r0[d]) + __uint_as_float(r1[d]) : __uint_as_float(r0[d]));
       }
     }
     tc_fence_before();
@@ -910,6 +918,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   long long* const trace = blockIdx.x == 0 ? g_attn_trace : nullptr;   // debug timeline
+  if (g_attn_trace != nullptr && tid == 0) {   // per-CTA start / end stamps
+    long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    g_attn_trace[512 + blockIdx.x * 2] = t0;
+  }
 
   if (tid == 0) {
     for (int w = 0; w < 2; ++w) {
@@ -962,6 +975,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (g_attn_trace != nullptr && tid == 0) {
+    long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    g_attn_trace[512 + blockIdx.x * 2 + 1] = t1;
+  }
   if (warp == 10) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);

@@ -50,7 +50,16 @@ struct VqWorkspace {
                       // {item, n (-1: scan the records), candidate codes ...}
   int* rr_count;      // [1]
   int* row_tok;       // [M] source row -> token (-1: not a token row); run mode over pre-split rows
+  // run-mode items that need an exact scan of every code (a part's candidate list overflowed,
+  // or > 8 candidates): split over kOvSub code ranges scanned by different warps of the re-rank
+  // kernel; the warp finishing an item's last range reduces the partial argmins
+  int* ov_list;       // [kOvCap] items
+  int* ov_count;      // [2] items listed, range units claimed
+  int* ov_done;       // [kOvCap] ranges finished per item
+  double* ov_d;       // [kOvCap * kOvSub] partial best distance
+  int* ov_k;          // [kOvCap * kOvSub] partial best code
 };
+constexpr int kOvCap = 1024, kOvSub = 16;
 
 static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -73,6 +82,11 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
   size_t o_rl = take((size_t)G * M * kRREntry * 4);
   size_t o_rc = take(4);
   size_t o_rt = take((size_t)M * 4);
+  size_t o_ol = take((size_t)kOvCap * 4);
+  size_t o_oc = take(8);
+  size_t o_od = take((size_t)kOvCap * 4);
+  size_t o_odd = take((size_t)kOvCap * kOvSub * 8);
+  size_t o_ok = take((size_t)kOvCap * kOvSub * 4);
   if (w && base) {
     uint8_t* b = reinterpret_cast<uint8_t*>(base);
     w->x_hi = reinterpret_cast<__nv_bfloat16*>(b + o_hi);
@@ -86,6 +100,11 @@ static size_t carve(VqWorkspace* w, void* base, int M, int G, int K, int gdp) {
     w->rr_list = reinterpret_cast<int*>(b + o_rl);
     w->rr_count = reinterpret_cast<int*>(b + o_rc);
     w->row_tok = reinterpret_cast<int*>(b + o_rt);
+    w->ov_list = reinterpret_cast<int*>(b + o_ol);
+    w->ov_count = reinterpret_cast<int*>(b + o_oc);
+    w->ov_done = reinterpret_cast<int*>(b + o_od);
+    w->ov_d = reinterpret_cast<double*>(b + o_odd);
+    w->ov_k = reinterpret_cast<int*>(b + o_ok);
   }
   return off;
 }
@@ -162,7 +181,11 @@ __global__ void vq_split_kernel(const float* __restrict__ x, int M, int ldx,
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   // the re-rank list is appended to by the GEMM epilogue that follows: reset here
-  if (blockIdx.x == 0 && threadIdx.x == 0) *w.rr_count = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *w.rr_count = 0;
+    w.ov_count[0] = 0;
+    w.ov_count[1] = 0;
+  }
   if (r >= M) return;
   const int src = rows ? rows[r] : r;
   const float* xr = x + (size_t)src * ldx;
@@ -195,7 +218,11 @@ __global__ void vq_split_v4_kernel(const float* __restrict__ x, int M, int ldx,
   const int r = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   // the re-rank list is appended to by the GEMM epilogue that follows: reset here
-  if (blockIdx.x == 0 && threadIdx.x == 0) *w.rr_count = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *w.rr_count = 0;
+    w.ov_count[0] = 0;
+    w.ov_count[1] = 0;
+  }
   if (r >= M) return;
   const int src = rows ? rows[r] : r;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)src * ldx);
@@ -232,11 +259,15 @@ __global__ void vq_split_v4_kernel(const float* __restrict__ x, int M, int ldx,
 
 // Inverse of the token -> source-row map for the run-mode GEMM over pre-split stack rows
 // (two launches: every row to -1, then the token rows; also resets the re-rank count).
-__global__ void vq_row_tok_fill_kernel(int* row_tok, int R, int* rr_count) {
+__global__ void vq_row_tok_fill_kernel(int* row_tok, int R, int* rr_count, int* ov_count) {
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r == 0) *rr_count = 0;
+  if (r == 0) {
+    *rr_count = 0;
+    ov_count[0] = 0;
+    ov_count[1] = 0;
+  }
   if (r < R) row_tok[r] = -1;
 }
 __global__ void vq_row_tok_scatter_kernel(const int32_t* __restrict__ rows, int M, int* row_tok) {
@@ -279,7 +310,10 @@ struct VqEpilogue {
     const int lane = threadIdx.x & 31;
     // the re-rank list count for the finalize kernel that follows (stream order): reset by
     // one thread here instead of a memset node in front of this GEMM
-    if (tc.m_blk == 0 && tc.n_blk == 0 && g == 0 && row_in_tile == 0 && cb == 0) *w.rr_count = 0;
+    if (tc.m_blk == 0 && tc.n_blk == 0 && g == 0 && row_in_tile == 0 && cb == 0) {
+      *w.rr_count = 0;
+      w.ov_count[0] = 0;   // (no overflow list in records mode)
+    }
     const float xn = ok ? w.x_norm[(size_t)g * M + row] : 0.f;
     const float a = window_a(xn);
     // pass 1: U = min_j (s_j + D_j)
@@ -442,8 +476,14 @@ struct VqRunEpilogue {
     }
     const uint32_t s_scs = smem_u32(stage);
     __syncwarp();   // the previous tile's reads of the staged terms are done
-    sts_v4(s_scs + 16 * lane, c0);
-    sts_v4(s_scs + 512 + 16 * lane, c1);
+    // SoA: [0, 256) ||c||^2, [256, 512) ||c||, [512, 768) eps ||c||^2 of the part's <= 64 codes
+    // (the common path reads four ||c||^2 per 16-byte load)
+    sts_f32(s_scs + 4 * lane, c0.x);
+    sts_f32(s_scs + 256 + 4 * lane, c0.y);
+    sts_f32(s_scs + 512 + 4 * lane, c0.z);
+    sts_f32(s_scs + 128 + 4 * lane, c1.x);
+    sts_f32(s_scs + 384 + 4 * lane, c1.y);
+    sts_f32(s_scs + 640 + 4 * lane, c1.z);
     __syncwarp();
   }
 
@@ -467,21 +507,34 @@ struct VqRunEpilogue {
 #pragma unroll 1
     for (int c0 = cb; c0 < ce; c0 += 32) {
       const int col0 = col_base + c0;
-      const uint32_t s_scs = s_stage + (c0 - cb) * 16;   // this chunk's 32 staged terms
+      const uint32_t s_cn = s_stage + (c0 - cb) * 4;   // this chunk's 32 staged ||c||^2
       uint32_t r[32];
       tmem_ld32(taddr + c0, r);
-      tmem_ld_wait();
-      float m0 = INFINITY, m1 = INFINITY;
+      float cn[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {   // r[j] <- s_j = ||c_j||^2 - 2 x.c_j
-        const float sc = fmaf(-2.0f, __uint_as_float(r[j]), lds_f32(s_scs + 16 * j));
-        r[j] = __float_as_uint(sc);
-        if (j & 1) m1 = fminf(m1, sc); else m0 = fminf(m0, sc);
+      for (int q = 0; q < 8; ++q) {   // (shared-memory loads overlap the TMEM load)
+        const float4 v = lds_v4(s_cn + 16 * q);
+        cn[4 * q] = v.x;
+        cn[4 * q + 1] = v.y;
+        cn[4 * q + 2] = v.z;
+        cn[4 * q + 3] = v.w;
       }
-      st.smin = fminf(st.smin, fminf(m0, m1));
+      tmem_ld_wait();
+      // r[j] <- s_j = ||c_j||^2 - 2 x.c_j (the same single-rounding FMA per lane of FFMA2)
+      float m4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float2 sc = ffma2(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])),
+                                make_float2(-2.0f, -2.0f), make_float2(cn[j], cn[j + 1]));
+        r[j] = __float_as_uint(sc.x);
+        r[j + 1] = __float_as_uint(sc.y);
+        m4[(j >> 1) & 3] = fmin3(m4[(j >> 1) & 3], sc.x, sc.y);
+      }
+      const float cmin = fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3]));
+      st.smin = fminf(st.smin, cmin);
       // + a rounding margin of 2^-21 (|smin| + 2 Dmax): the comparisons stay exact supersets
       const float thr = (st.smin + dmax2) + kEps * (fabsf(st.smin) + dmax2);
-      if (fminf(m0, m1) > thr) continue;   // common case: nothing in this chunk can compete
+      if (cmin > thr) continue;   // common case: nothing in this chunk can compete
       uint32_t m = 0;
 #pragma unroll
       for (int j = 0; j < 32; ++j) m |= (__uint_as_float(r[j]) <= thr ? 1u : 0u) << j;
@@ -489,8 +542,8 @@ struct VqRunEpilogue {
         const int j = __ffs(m) - 1;
         m &= m - 1;
         const float sc = pick32(r, j);
-        const float4 q = lds_v4(s_scs + 16 * j);
-        const float d = fmaf(a, q.y, q.z);
+        const uint32_t o = (uint32_t)(c0 - cb + j) * 4;
+        const float d = fmaf(a, lds_f32(s_stage + 256 + o), lds_f32(s_stage + 512 + o));
         const float up = sc + d + 1e-30f, lo = sc - d;
         if (up < st.U) {   // tighter bound: prune the kept codes
           st.U = up;
@@ -565,16 +618,25 @@ struct VqRunEpilogue {
       if (n == 1 && !ovf) {
         idx_out[(size_t)tok * G + g] = only;
       } else {
-        const int slot = atomicAdd(w.rr_count, 1);
-        int* ent = w.rr_list + (size_t)slot * kRREntry;
-        ent[0] = g * Mtok + tok;
-        if (!ovf && n >= 1 && n <= 8) {
-          ent[1] = n;
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (i < n) ent[2 + i] = list[i];
+        const bool direct = !ovf && n >= 1 && n <= 8;
+        // exact scan of every code: split over the re-rank kernel's warps (ov list) while it
+        // has room, else one warp scans the whole group (-2 entry)
+        const int os = direct ? kOvCap : atomicAdd(w.ov_count, 1);
+        if (os < kOvCap) {
+          w.ov_list[os] = g * Mtok + tok;
+          w.ov_done[os] = 0;
         } else {
-          ent[1] = -2;                          // full fp64 scan of the group's codes
+          const int slot = atomicAdd(w.rr_count, 1);
+          int* ent = w.rr_list + (size_t)slot * kRREntry;
+          ent[0] = g * Mtok + tok;
+          if (direct) {
+            ent[1] = n;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i < n) ent[2 + i] = list[i];
+          } else {
+            ent[1] = -2;                        // full fp64 scan of the group's codes
+          }
         }
       }
     }
@@ -660,7 +722,8 @@ __device__ __forceinline__ void vq_decide(const AstraCodebook& cb, const float* 
         }
     }
   } else {
-    overflow = 1;   // wide codebooks: the re-rank kernel scans the records
+    // wide codebooks (> 32 records per row): a single surviving candidate still decides here;
+    // several go to the re-rank kernel, which scans the records (no compacted list)
     for (int c = lane; c < nchunk; c += 32) best = fminf(best, w.rec_best[rec0 + c]);
     for (int o = 16; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
     for (int c = lane; c < nchunk; c += 32) {
@@ -680,7 +743,8 @@ __device__ __forceinline__ void vq_decide(const AstraCodebook& cb, const float* 
     only = min(only, __shfl_xor_sync(0xffffffffu, only, o));
     overflow |= __shfl_xor_sync(0xffffffffu, overflow, o);
   }
-  if (inline_rr && !overflow && n > 1 && n <= kRRCands) {
+  const bool wide = nchunk > 32;   // no per-lane candidate slots (ix / live) were filled
+  if (inline_rr && !wide && !overflow && n > 1 && n <= kRRCands) {
     // several window candidates: the warp re-ranks them now, exact fp64 with the reference's
     // expression (||p||^2 - 2 p.c) + ||c||^2, ties to the lowest index
     const int gd = cb.group_dim, K = cb.size;
@@ -714,7 +778,7 @@ __device__ __forceinline__ void vq_decide(const AstraCodebook& cb, const float* 
     if (lane == 0) slot = atomicAdd(w.rr_count, 1);
     slot = __shfl_sync(0xffffffffu, slot, 0);
     int* ent = w.rr_list + (size_t)slot * kRREntry;
-    const bool direct = !overflow && n <= kRRCands;
+    const bool direct = !wide && !overflow && n <= kRRCands;
     if (direct) {
       const int cnt = __popc(live);
       int pre = cnt;
@@ -774,7 +838,7 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
                                                         int rec_by_row, int part_codes) {
   pdl_wait();
   pdl_trigger();
-  __shared__ int s_cand[8][32 * kVqCap];
+  __shared__ __align__(16) int s_cand[8][32 * kVqCap];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int G = cb.groups, K = cb.size, gd = cb.group_dim;
   const int total = *w.rr_count;
@@ -891,7 +955,63 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
       pp = warp_sum_d(pp);
       double bd = INFINITY;
       int bi = 0x7FFFFFFF;
-      if (gd <= 32 * kVqCap) {
+      if (gd <= 32 * kVqCap && gd % 4 == 0) {
+        // narrow groups, 16-byte rows: lane k scores codes k, k + 32, ... with float4 loads of
+        // the code row (4 in flight per code, two codes per step) against the token slice
+        // broadcast from shared memory
+        float* xsh = reinterpret_cast<float*>(s_cand[wib]);
+        for (int e = lane; e < gd; e += 32) xsh[e] = __ldg(xr + e);
+        __syncwarp();
+        const int q4 = gd >> 2;
+        const float4* c4 = reinterpret_cast<const float4*>(cents);
+        const float4* x4 = reinterpret_cast<const float4*>(xsh);
+        for (int k = lane; k < K; k += 64) {
+          const int k2 = min(k + 32, K - 1);
+          const float4* ca = c4 + (size_t)k * q4;
+          const float4* cb2 = c4 + (size_t)k2 * q4;
+          double pa = 0.0, pb = 0.0;
+          for (int q = 0; q < q4; q += 4) {
+            float4 va[4], vb[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              va[i] = q + i < q4 ? __ldg(ca + q + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+              vb[i] = q + i < q4 ? __ldg(cb2 + q + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (q + i >= q4) break;
+              const float4 xv = x4[q + i];
+              pa = fma((double)xv.x, (double)va[i].x, pa);
+              pa = fma((double)xv.y, (double)va[i].y, pa);
+              pa = fma((double)xv.z, (double)va[i].z, pa);
+              pa = fma((double)xv.w, (double)va[i].w, pa);
+              pb = fma((double)xv.x, (double)vb[i].x, pb);
+              pb = fma((double)xv.y, (double)vb[i].y, pb);
+              pb = fma((double)xv.z, (double)vb[i].z, pb);
+              pb = fma((double)xv.w, (double)vb[i].w, pb);
+            }
+          }
+          const double d = (pp - 2.0 * pa) + cb.c_sq64[(size_t)g * K + k];
+          if (d < bd) {   // ascending k per lane: strict < keeps the lowest index
+            bd = d;
+            bi = k;
+          }
+          const double d2 = (pp - 2.0 * pb) + cb.c_sq64[(size_t)g * K + k2];
+          if (k + 32 < K && d2 < bd) {
+            bd = d2;
+            bi = k2;
+          }
+        }
+        __syncwarp();
+        for (int o = 16; o; o >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+          const int ok_ = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (od < bd || (od == bd && ok_ < bi)) {
+            bd = od;
+            bi = ok_;
+          }
+        }
+      } else if (gd <= 32 * kVqCap) {
         float* xsh = reinterpret_cast<float*>(s_cand[wib]);
         for (int e = lane; e < gd; e += 32) xsh[e] = __ldg(xr + e);
         __syncwarp();
@@ -1038,6 +1158,110 @@ __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const 
     if (lane == 0) {
       idx_out[(size_t)row * G + g] = bi;
       if (stats) atomicAdd(&stats[overflowed ? 1 : 0], 1);
+    }
+  }
+  // Exact scans of the overflow list (run mode): unit u = (item u / kOvSub, code range
+  // u % kOvSub), claimed by warps as they finish their entries.  Each range's fp64 argmin goes
+  // to ov_d / ov_k; the warp completing an item's last range reduces them in range order
+  // (lowest code on equal distance, as the reference's argmin).
+  const int n_ov = min(w.ov_count[0], kOvCap);
+  if (n_ov == 0) return;
+  const int sc = (K + kOvSub - 1) / kOvSub;
+  while (true) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(&w.ov_count[1], 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= n_ov * kOvSub) break;
+    const int slot = u / kOvSub, sub = u % kOvSub;
+    const int item = __ldcg(w.ov_list + slot);
+    const int g = item / M, row = item % M;
+    const int src = rows ? rows[row] : row;
+    const float* xr = x + (size_t)src * ldx + (size_t)g * gd;
+    const float* cents = cb.centroids + (size_t)g * K * gd;
+    const double* cc = cb.c_sq64 + (size_t)g * K;
+    const int k_lo = sub * sc, k_hi = min(K, k_lo + sc);
+    double pp = 0.0;
+    for (int e = lane; e < gd; e += 32) pp = fma((double)__ldg(xr + e), (double)__ldg(xr + e), pp);
+    pp = warp_sum_d(pp);
+    double bd = INFINITY;
+    int bi = 0x7FFFFFFF;
+    if (gd <= 32 * kVqCap && gd % 4 == 0) {
+      // lanes over codes, token slice broadcast from shared memory, 16-byte code-row loads
+      float* xsh = reinterpret_cast<float*>(s_cand[wib]);
+      __syncwarp();
+      for (int e = lane; e < gd; e += 32) xsh[e] = __ldg(xr + e);
+      __syncwarp();
+      const int q4 = gd >> 2;
+      const float4* x4 = reinterpret_cast<const float4*>(xsh);
+      for (int k = k_lo + lane; k < k_hi; k += 32) {
+        const float4* c4 = reinterpret_cast<const float4*>(cents + (size_t)k * gd);
+        double pc = 0.0;
+        for (int q = 0; q < q4; q += 4) {
+          float4 v[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[i] = q + i < q4 ? __ldg(c4 + q + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (q + i >= q4) break;
+            const float4 xv = x4[q + i];
+            pc = fma((double)xv.x, (double)v[i].x, pc);
+            pc = fma((double)xv.y, (double)v[i].y, pc);
+            pc = fma((double)xv.z, (double)v[i].z, pc);
+            pc = fma((double)xv.w, (double)v[i].w, pc);
+          }
+        }
+        const double d = (pp - 2.0 * pc) + cc[k];
+        if (d < bd) {   // ascending k per lane
+          bd = d;
+          bi = k;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+        const int ok_ = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (od < bd || (od == bd && ok_ < bi)) {
+          bd = od;
+          bi = ok_;
+        }
+      }
+      __syncwarp();
+    } else {
+      for (int k = k_lo; k < k_hi; ++k) {   // lanes over the dimensions
+        const double d = exact_d2(xr, cents + (size_t)k * gd, gd, pp, cc[k], lane);
+        if (d < bd) {
+          bd = d;
+          bi = k;
+        }
+      }
+    }
+    int last = 0;
+    if (lane == 0) {
+      w.ov_d[u] = bd;
+      w.ov_k[u] = bi;
+      __threadfence();
+      last = atomicAdd(w.ov_done + slot, 1) == kOvSub - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence();
+      double d = INFINITY;
+      int k = 0x7FFFFFFF;
+      if (lane < kOvSub) {
+        d = __ldcg(w.ov_d + (size_t)slot * kOvSub + lane);
+        k = __ldcg(w.ov_k + (size_t)slot * kOvSub + lane);
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, d, o);
+        const int ok_ = __shfl_xor_sync(0xffffffffu, k, o);
+        if (od < d || (od == d && ok_ < k)) {
+          d = od;
+          k = ok_;
+        }
+      }
+      if (lane == 0) {
+        idx_out[(size_t)row * G + g] = k;
+        if (stats) atomicAdd(&stats[1], 1);
+      }
     }
   }
 }
@@ -1208,7 +1432,10 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
   // pair for ceil(K / 256) tiles; with fewer row blocks than pairs the idle SMs cost more than
   // the finalize pass saves — ViT-B B=64: 50 blocks on 74 pairs, 58 us vs 51 + 9)
   const long pairs = num_sms() / 2, rblocks = (Mg + 2 * kBM - 1) / (2 * kBM), ct = (K + kVqBN - 1) / kVqBN;
-  const bool run_g1 = rec_by_row && cluster == 2 && K >= kVqBN &&
+  // (and only up to K = 1024: a run keeps 4 candidate slots per 1/4 of the codebook, and an
+  // overflow costs an exact scan of every code — ViT-L K = 4096 saw 25 per step, 5 ms per layer;
+  // records bound an overflow to its 64-code part)
+  const bool run_g1 = rec_by_row && cluster == 2 && K >= kVqBN && K <= 4 * kVqBN &&
                       ((rblocks + pairs - 1) / pairs) * ct <= (rblocks * ct + pairs - 1) / pairs;
   if (G > 1 || run_g1) {
     // Run mode: grouped codebooks (token-gathered operands), and G = 1 over the pre-split stack
@@ -1216,11 +1443,11 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
     // no records, no finalize pass; the re-rank takes the ~5% multi-candidate rows).
     const int* row_tok = row_tok_in;
     if (rec_by_row && !row_tok) {
-      launch_k(vq_row_tok_fill_kernel, (Mg + 255) / 256, 256, 0, s, w.row_tok, Mg, w.rr_count);
+      launch_k(vq_row_tok_fill_kernel, (Mg + 255) / 256, 256, 0, s, w.row_tok, Mg, w.rr_count, w.ov_count);
       launch_k(vq_row_tok_scatter_kernel, (M + 255) / 256, 256, 0, s, rows, M, w.row_tok);
       row_tok = w.row_tok;
     } else if (rec_by_row) {   // the caller's map: only the re-rank list count to reset
-      launch_k(vq_row_tok_fill_kernel, 1, 32, 0, s, w.row_tok, 0, w.rr_count);
+      launch_k(vq_row_tok_fill_kernel, 1, 32, 0, s, w.row_tok, 0, w.rr_count, w.ov_count);
     }
     const long runs = (long)G * ((Mg + kBM * cluster - 1) / (kBM * cluster));
     const int rbn = (K <= kVqBNMin || (G > 1 && runs * cluster < num_sms())) ? kVqBNMin : kVqBN;

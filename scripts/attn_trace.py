@@ -24,7 +24,7 @@ rt = AstraRuntime(params, cluster.partition_tokens(196, n), batch=64, precision=
 rt.stage_input(xs)
 rt.forward()
 torch.cuda.synchronize()
-buf = torch.zeros(32 * 16, dtype=torch.int64, device="cuda")
+buf = torch.zeros(512 + 2 * 1024, dtype=torch.int64, device="cuda")
 lib = _native.load()
 lib.astra_attention_trace(buf.data_ptr())
 rt.profile = {}
@@ -33,7 +33,15 @@ torch.cuda.synchronize()
 lib.astra_attention_trace(None)
 ms = [s.elapsed_time(e) for s, e in rt.profile["attention"]]
 print("attention ms", ms)
-t = buf.view(32, 16).cpu().numpy().astype(np.int64)
+allb = buf.cpu().numpy().astype(np.int64)
+t = allb[:512].reshape(32, 16)
+se = allb[512:].reshape(-1, 2)
+se = se[se[:, 0] > 0]
+c0 = se[:, 0].min()
+st, en = (se[:, 0] - c0) / 1000, (se[:, 1] - c0) / 1000
+print(f"CTAs {len(se)}: start min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f} us, "
+      f"end min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f} us")
+print("end histogram (us):", np.histogram(en, bins=8)[0].tolist(), np.round(np.histogram(en, bins=8)[1], 1).tolist())
 t0 = t[t > 0].min()
 names = ["0p2end", "0S", "0PV", "0sm_st", "0sm_end", "0Sdone", "0p1end", "0top", "1p2end", "1S", "1PV", "1sm_st", "1sm_end", "1Sdone", "1p1end", "1top"]
 print("unit " + " ".join(f"{x:>8s}" for x in names))

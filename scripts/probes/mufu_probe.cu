@@ -22,6 +22,17 @@ __global__ void ex2bf(float* out, int iters) {
   for (int k = 0; k < 8; ++k) s += a[k];
   out[blockIdx.x * blockDim.x + threadIdx.x] = (float)s;
 }
+__global__ void ex2h(float* out, int iters) {
+  unsigned a[8];
+  for (int k = 0; k < 8; ++k) a[k] = 0x3c003c00u + threadIdx.x + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(a[k]));
+  }
+  unsigned s = 0;
+  for (int k = 0; k < 8; ++k) s += a[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)s;
+}
 int main() {
   float* o;
   cudaMalloc(&o, 148 * 1024 * 4 * 8);
@@ -44,6 +55,13 @@ int main() {
     cudaEventSynchronize(e);
     cudaEventElapsedTime(&ms, s, e);
     printf("bf16x2 ex2: threads/SM %d: %.3f ms, %.1f instr/clk/SM (x2 values)\n", threads, ms, ops / (ms * 1e-3) / 148 / 1.965e9);
+    ex2h<<<148, threads>>>(o, iters);
+    cudaEventRecord(s);
+    ex2h<<<148, threads>>>(o, iters);
+    cudaEventRecord(e);
+    cudaEventSynchronize(e);
+    cudaEventElapsedTime(&ms, s, e);
+    printf("f16x2 ex2: threads/SM %d: %.3f ms, %.1f instr/clk/SM (x2 values)\n", threads, ms, ops / (ms * 1e-3) / 148 / 1.965e9);
   }
   return 0;
 }

@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(288, 1) k(long long* out, int batches, int mod
       long long t0 = clock64();
       int nw = 0;
       for (int b = 0; b < batches; ++b) {
-        if (mode >= 128) {   // 13 SS MMAs 128 x N x 16, K-major A and B, N = mode - 128
+        if (mode >= 128 && mode < 256) {   // 13 SS MMAs 128 x N x 16, K-major A and B, N = mode - 128
           const int N = mode - 128;
           for (int kk = 0; kk < 13; ++kk)
             umma_f16(tmem + 256, sdesc_kmajor_sw128(a_s + (kk & 3) * 32), sdesc_kmajor_sw128(v_s + (kk & 3) * 32),
@@ -43,7 +43,10 @@ __global__ void __launch_bounds__(288, 1) k(long long* out, int batches, int mod
                      idesc_bf16_f32(128, 208), kk > 0);
         } else {
           for (int kk = 0; kk < 13; ++kk) {
-            if (mode & 2)
+            if ((mode & 2) && (mode & 256))   // SS, K-major A (P) and K-major B (V^T)
+              umma_f16(tmem + 384, sdesc_kmajor_sw128(a_s + (kk >> 2) * 16384 + (kk & 3) * 32),
+                       sdesc_kmajor_sw128(v_s + (kk >> 2) * 8192 + (kk & 3) * 32), idesc_bf16_f32(128, 64), kk > 0);
+            else if (mode & 2)
               umma_f16(tmem + 384, sdesc_kmajor_sw128(a_s + (kk >> 2) * 16384 + (kk & 3) * 32),
                        sdesc_mnmajor_sw128(v_s + kk * 2048, 8192), idesc_bmn(128, 64), kk > 0);
             else if (mode & 8)   // two independent accumulators
@@ -60,7 +63,7 @@ __global__ void __launch_bounds__(288, 1) k(long long* out, int batches, int mod
                           idesc_bmn(128, 64), kk > 0);
           }
         }
-        if ((mode & 64) == 0 || mode >= 128 || (b & 7) == 7) {
+        if ((mode & 64) == 0 || (mode >= 128 && mode < 256) || (b & 7) == 7) {
           umma_commit(&bar);
           mbar_wait_spin(&bar, nw & 1);
           ++nw;
@@ -114,6 +117,19 @@ int main() {
     long long h;
     cudaMemcpy(&h, o, 8, cudaMemcpyDeviceToHost);
     printf("13 x SS 128x%dx16 (commit+wait per batch): %lld cycles\n", N, h);
+  }
+  {
+    const char* xn[] = {"PV TS Kmajor B no-wait", "PV SS Kmajor B no-wait", "PV TS Kmajor B +sm nw", "PV SS Kmajor B +sm nw",
+                        "PV TS 2 accum no-wait", "PV TS 4 accum no-wait"};
+    const int xm[] = {64 | 32, 64 | 256 | 2, 64 | 32 | 1, 64 | 256 | 2 | 1, 64 | 8, 64 | 16};
+    for (int i = 0; i < 6; ++i) {
+      k<<<148, 288, smem>>>(o, 2000, xm[i]);
+      k<<<148, 288, smem>>>(o, 2000, xm[i]);
+      cudaDeviceSynchronize();
+      long long h;
+      cudaMemcpy(&h, o, 8, cudaMemcpyDeviceToHost);
+      printf("%-22s %lld cycles per batch\n", xn[i], h);
+    }
   }
   for (int m = 9; m < 13; ++m) {
     k<<<148, 288, smem>>>(o, 2000, modes[m]);
