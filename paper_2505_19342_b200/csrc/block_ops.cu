@@ -22,6 +22,7 @@ struct LnGather {
   const int32_t* idx;     // [M, G]
   int G, K, gd;
   int32_t* err;
+  uint32_t per_magic;     // ceil(2^32 / (gd / 4)): q / (gd / 4) = umulhi(q, magic) for q < 2^8
 };
 
 template <int VPL>  // float4 vectors per lane (D = VPL * 128)
@@ -45,7 +46,7 @@ __global__ void layernorm_kernel(const float* __restrict__ x, int M, int ldx,
       const int per = gat.gd >> 2;   // float4s per group
 #pragma unroll
       for (int i = 0; i < VPL; ++i) {
-        const int q = lane + 32 * i, g = q / per;
+        const int q = lane + 32 * i, g = per == 1 ? q : (int)__umulhi((uint32_t)q, gat.per_magic);
         const int k = __ldg(gat.idx + (size_t)row * gat.G + g);
         if (k < 0 || k >= gat.K) {
           atomicExch(gat.err, 1);
@@ -467,7 +468,9 @@ extern "C" int astra_vq_decode_layernorm(const AstraCodebook* cbp, const int32_t
   cudaStream_t s = as_stream(stream);
   auto hi = reinterpret_cast<__nv_bfloat16*>(out_hi);
   auto lo = reinterpret_cast<__nv_bfloat16*>(out_lo);
-  const LnGather gat{cb.centroids, idx, cb.groups, cb.size, cb.group_dim, err_flag};
+  const uint32_t per = (uint32_t)(cb.group_dim / 4);
+  const LnGather gat{cb.centroids, idx, cb.groups, cb.size, cb.group_dim, err_flag,
+                     (uint32_t)((0x100000000ull + per - 1) / per)};
   const int grid1 = (M + 3) / 4;
   if (D == 768)
     launch_k(layernorm_kernel<6>, grid1, 128, 0, s, nullptr, M, 0, gain, bias, eps, nullptr, 0, hi, lo,

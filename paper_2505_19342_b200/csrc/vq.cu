@@ -1294,6 +1294,29 @@ __global__ void vq_decode_kernel(AstraCodebook cb, const int32_t* __restrict__ i
   }
 }
 
+// 16-byte form (gd % 4 == 0, aligned rows): one thread per output float4, so narrow groups
+// (gd = 24..64: 6..16 float4 per group) keep every lane busy and a warp stores 512 contiguous
+// bytes of a row; the code of (m, g) is a broadcast load shared by the group's threads.
+__global__ void vq_decode_v4_kernel(AstraCodebook cb, const int32_t* __restrict__ idx, int M,
+                                    float* __restrict__ out, int ldo, int32_t* err,
+                                    uint32_t per_magic) {
+  pdl_wait();
+  pdl_trigger();
+  const int G = cb.groups, K = cb.size, gd = cb.group_dim;
+  const int row4 = (G * gd) >> 2, per = gd >> 2;
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)M * row4) return;
+  const int m = (int)(t / row4), c4 = (int)(t - (long)m * row4);
+  const int g = per == 1 ? c4 : (int)__umulhi((uint32_t)c4, per_magic);   // (magic wraps for 1)
+  const int k = __ldg(idx + (size_t)m * G + g);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (k < 0 || k >= K)
+    atomicExch(err, 1);
+  else
+    v = __ldg(reinterpret_cast<const float4*>(cb.centroids + ((size_t)g * K + k) * gd) + (c4 - g * per));
+  *(reinterpret_cast<float4*>(out + (size_t)m * ldo) + c4) = v;
+}
+
 // ------------------------------------------------------------ packing
 __global__ void pack_kernel(const int32_t* __restrict__ idx, int count, int bits,
                             uint32_t* __restrict__ words, int nwords) {
@@ -1548,7 +1571,16 @@ extern "C" int astra_vq_decode(const AstraCodebook* cbp, const int32_t* idx, int
   ASTRA_REQUIRE(ldo >= cb.groups * cb.group_dim, ASTRA_ERR_SHAPE, "astra_vq_decode: ldo too small");
   if (M == 0) return ASTRA_OK;
   const int items = M * cb.groups;
-  launch_k(vq_decode_kernel, (items + 7) / 8, 256, 0, as_stream(stream), cb, idx, M, out, ldo, err_flag);
+  const int D = cb.groups * cb.group_dim;
+  if (cb.group_dim % 4 == 0 && ldo % 4 == 0 && D / 4 <= (1 << 20) &&
+      ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(cb.centroids)) & 15) == 0) {
+    const uint32_t per = (uint32_t)(cb.group_dim / 4);
+    const long threads = (long)M * (D / 4);
+    launch_k(vq_decode_v4_kernel, (unsigned)((threads + 255) / 256), 256, 0, as_stream(stream), cb,
+             idx, M, out, ldo, err_flag, (uint32_t)((0x100000000ull + per - 1) / per));
+  } else {
+    launch_k(vq_decode_kernel, (items + 7) / 8, 256, 0, as_stream(stream), cb, idx, M, out, ldo, err_flag);
+  }
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;
 }
