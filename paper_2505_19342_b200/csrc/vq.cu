@@ -1572,7 +1572,8 @@ extern "C" int astra_vq_decode(const AstraCodebook* cbp, const int32_t* idx, int
   if (M == 0) return ASTRA_OK;
   const int items = M * cb.groups;
   const int D = cb.groups * cb.group_dim;
-  if (cb.group_dim % 4 == 0 && ldo % 4 == 0 && D / 4 <= (1 << 20) &&
+  // (wide groups keep the warp per (m, g): 32+ float4 per code already fill the warp)
+  if (cb.group_dim < 128 && cb.group_dim % 4 == 0 && ldo % 4 == 0 && D / 4 <= (1 << 20) &&
       ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(cb.centroids)) & 15) == 0) {
     const uint32_t per = (uint32_t)(cb.group_dim / 4);
     const long threads = (long)M * (D / 4);
