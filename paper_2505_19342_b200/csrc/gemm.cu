@@ -56,6 +56,11 @@ struct StdEpilogueT {
   int gelu;
   int BN;
   int vec;  // all row pitches / bases allow 16-byte vectors
+  // bf16-only outputs of the specialised epilogues (Q|K|V, W1): the warp's 32x16 chunk goes
+  // out as one TMA store from a row-major staging buffer (two per warp, alternating) instead of
+  // a shared-memory round trip and per-lane global stores
+  static constexpr bool kTmaOut = kF != 0 && (kF & kEpHi) && !(kF & (kEpF32 | kEpLo));
+  alignas(64) CUtensorMap tm_hi;   // out_hi [M, N], box 32 rows x 16 columns (set by the host)
 
   __device__ __forceinline__ void store_bf16(uint8_t* stage, __nv_bfloat16* out, int row0,
                                              int col0, const uint32_t (&h)[8]) const {
@@ -229,7 +234,24 @@ struct StdEpilogueT {
             lp[j >> 1] = *reinterpret_cast<uint32_t*>(&l2);
           }
         }
-        if (fast) {
+        if (kTmaOut && fast) {
+          // TMA needs a 128-byte aligned source: warp stages are 2112 B apart, so odd warps'
+          // buffers start 64 B in (the stage's last 64 B are free: the bias is in registers)
+          const uint32_t s0 = smem_u32(stage);
+          const uint32_t buf = ((s0 + 127u) & ~127u) + (((c0 - cb) >> 4) & 1) * 1024;
+          if (lane == 0) bulk_wait_read<1>();   // the store that read this buffer is done
+          __syncwarp();
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 32), "r"(hp[0]),
+                       "r"(hp[1]), "r"(hp[2]), "r"(hp[3]) : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(buf + lane * 32 + 16),
+                       "r"(hp[4]), "r"(hp[5]), "r"(hp[6]), "r"(hp[7]) : "memory");
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tm_hi, buf, col0, row0);
+            bulk_commit();
+          }
+        } else if (fast) {
           store_bf16(stage, out_hi, row0, col0, hp);
           if (has_lo) store_bf16(stage, out_lo, row0, col0, lp);
         } else if (row_ok) {
@@ -282,6 +304,11 @@ static int launch_spec(int BN, const CUtensorMap& ta, const CUtensorMap& talo,
                        const StdEpilogue& g, cudaStream_t stream) {
   StdEpilogueT<kF> epi{g.M, g.N, g.bias, g.residual, g.ld_res, g.out_f32, g.ld_f32, g.out_hi,
                        g.out_lo, g.ld_bf, g.gelu, BN, g.vec};
+  if constexpr (StdEpilogueT<kF>::kTmaOut) {
+    const int st = make_tmap_2d(&epi.tm_hi, g.out_hi, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, g.M, g.N,
+                                g.ld_bf, 32, 16, false);
+    if (st) return st;
+  }
   TileSched sched{(M + kBM - 1) / kBM, (N + BN - 1) / BN, 1, 1};
   const cudaError_t e =
       BN == 256 ? launch_tc_gemm<256, 1, gemm_stages<256, 1, 2>(), 2>(ta, talo, tb, tblo, K, sched,

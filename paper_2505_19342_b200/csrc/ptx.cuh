@@ -110,6 +110,23 @@ ASTRA_DEVICE void tma_gather4(void* smem_dst, const void* desc, uint64_t* bar, i
       "r"(r2), "r"(r3)
       : "memory");
 }
+// 2-D tiled store smem -> global (bulk group): rows / columns past the tensor are not written.
+ASTRA_DEVICE void tma_store_2d(const void* desc, uint32_t smem_src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(desc)),
+               "r"(smem_src), "r"(c0), "r"(c1)
+               : "memory");
+}
+ASTRA_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// at most N committed bulk groups may still be reading their shared-memory source
+template <int N>
+ASTRA_DEVICE void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+ASTRA_DEVICE void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 // 3-D tiled load: (inner, mid, outer).
 ASTRA_DEVICE void tma_load_3d(void* smem_dst, const void* desc, uint64_t* bar, int c0, int c1,
                               int c2, uint64_t cache_hint) {

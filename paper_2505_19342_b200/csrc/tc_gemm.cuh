@@ -139,7 +139,8 @@ template <int BN, int PASSES, int STAGES, int CLUSTER, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAlo,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBlo,
-                   int K, TileSched sched, int a_batch_rows, int b_batch_rows, Epi epi) {
+                   int K, TileSched sched, int a_batch_rows, int b_batch_rows,
+                   const __grid_constant__ Epi epi) {
   using S = GemmSmem<BN, PASSES, CLUSTER>;
   static_assert(CLUSTER == 1 || CLUSTER == 2 || CLUSTER == 4, "cluster of 1, 2 or 4");
   constexpr bool kPair = CLUSTER >= 2;
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait<0>();   // epilogues that store by TMA: complete before exit
   }
 
   tc_fence_before();
