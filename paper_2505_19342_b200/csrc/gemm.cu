@@ -310,11 +310,14 @@ static int launch_spec(int BN, const CUtensorMap& ta, const CUtensorMap& talo,
     if (st) return st;
   }
   TileSched sched{(M + kBM - 1) / kBM, (N + BN - 1) / BN, 1, 1};
+  // (BN = 128: one rank's few token rows at N >= 8 — the generic epilogue spilled there)
   const cudaError_t e =
       BN == 256 ? launch_tc_gemm<256, 1, gemm_stages<256, 1, 2>(), 2>(ta, talo, tb, tblo, K, sched,
                                                                       0, 0, epi, stream, num_sms())
-                : launch_tc_gemm<192, 1, gemm_stages<192, 1, 2>(), 2>(ta, talo, tb, tblo, K, sched,
-                                                                      0, 0, epi, stream, num_sms());
+      : BN == 192 ? launch_tc_gemm<192, 1, gemm_stages<192, 1, 2>(), 2>(ta, talo, tb, tblo, K, sched,
+                                                                        0, 0, epi, stream, num_sms())
+                  : launch_tc_gemm<128, 1, gemm_stages<128, 1, 2>(), 2>(ta, talo, tb, tblo, K, sched,
+                                                                        0, 0, epi, stream, num_sms());
   ASTRA_CUDA_CHECK(e);
   return ASTRA_OK;
 }
@@ -466,7 +469,7 @@ extern "C" int astra_gemm(const void* a_hi, const void* a_lo, int lda, const voi
                   ld_f32, reinterpret_cast<__nv_bfloat16*>(out_hi),
                   reinterpret_cast<__nv_bfloat16*>(out_lo), ld_bf, gelu, 0, vec};
   cudaStream_t s = as_stream(stream);
-  if (passes == 1 && cluster == 2 && vec && (BN == 256 || BN == 192)) {
+  if (passes == 1 && cluster == 2 && vec && (BN == 256 || BN == 192 || BN == 128)) {
     const int flags = (bias ? kEpBias : 0) | (gelu == 2 ? kEpGeluFast : 0) |
                       (gelu == 1 ? kEpGeluExact : 0) | (residual ? kEpResid : 0) |
                       (out_f32 ? kEpF32 : 0) | (out_hi ? kEpHi : 0) | (out_lo ? kEpLo : 0);
