@@ -26,6 +26,7 @@ CONFIGS = {
     "vitl": (24, 1024, 16, 1000, 576, 32, 1024, 1, False),
     "vitl_g16": (24, 1024, 16, 1000, 576, 32, 1024, 16, False),
     "vitl_g32": (24, 1024, 16, 1000, 576, 32, 1024, 32, False),
+    "gpt2m": (24, 1024, 16, 50257, 4096, 2, 1024, 1, True),   # BASELINE config #5
 }
 
 
@@ -47,12 +48,7 @@ def run(name, n, steps, warmup, rank=None):
     rt = AstraRuntime(params, plan, batch=B, mode="generate" if causal else "classify",
                       precision="fast", comm=comm)
     if causal:
-        ids = rng.integers(0, C, size=(B, T))
-        src = np.empty(rt.R, dtype=np.int32)
-        for (v, b), base in rt.row_base.items():
-            st, sz = rt.starts[v], rt.sizes[v]
-            src[base:base + sz] = ids[b, st:st + sz]
-        rt.row_src.copy_(torch.from_numpy(src))
+        rt.set_ids(rng.integers(0, C, size=(B, T)))
     else:
         rt.stage_input(data.make_classify_batch(D, T, B, seed=1))
     torch.cuda.synchronize()
