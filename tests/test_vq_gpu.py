@@ -33,7 +33,10 @@ def test_quantize_golden(cuda, i):
 
 @pytest.mark.parametrize("m,k,d,g,scale", [(6000, 1024, 768, 1, 1.0), (3000, 1024, 768, 16, 1.0),
                                            (2000, 1024, 768, 32, 0.3), (4000, 4096, 64, 1, 1.0),
-                                           (3000, 256, 1024, 1, 5.0), (513, 8, 32, 1, 1.0)])
+                                           (3000, 256, 1024, 1, 5.0), (513, 8, 32, 1, 1.0),
+                                           # wide codebooks: > 32 chunk records per row (G=1),
+                                           # run mode with 1024-code parts (G=16)
+                                           (3000, 4096, 1024, 1, 1.0), (2000, 4096, 1024, 16, 1.0)])
 def test_quantize_random_bit_exact(cuda, m, k, d, g, scale):
     from paper_2505_19342_b200 import vq
     rng = np.random.default_rng(m + k + d + g)
@@ -134,3 +137,41 @@ def test_decode_layernorm_equals_decode_then_layernorm(cuda, m, k, d, g):
                  gain.data_ptr(), bias.data_ptr(), 1e-5, hi.data_ptr(), None, d, err.data_ptr(), s)
     torch.cuda.synchronize()
     assert int(err[0]) == 1
+
+
+@pytest.mark.parametrize("g,m", [(16, 3000), (1, 2000)])
+def test_quantize_overflow_scans_bit_exact(cuda, g, m):
+    """Codebooks of near-duplicate codes: every token has ~16 codes inside the error window,
+    so candidate lists overflow — run mode (G=16) sends the items to the split exact scans
+    (more than the list capacity here, so the one-warp fallback runs too), records mode (G=1)
+    scans the overflowing 64-code parts.  Indices stay bit-identical to the fp64 argmin."""
+    from paper_2505_19342_b200 import vq
+    rng = np.random.default_rng(7 + g)
+    k, d = 1024, 1024
+    gd = d // g
+    cents = []
+    for _ in range(g):
+        base = rng.normal(size=(k // 16, gd))
+        cents.append((np.repeat(base, 16, axis=0) + rng.normal(size=(k, gd)) * 1e-5).astype(np.float32))
+    x = np.concatenate([c[rng.integers(0, k, size=m)] for c in cents], axis=1)
+    x = (x + rng.normal(size=(m, d)) * 1e-3).astype(np.float32)
+    dc = vq.DeviceCodebook(torch.from_numpy(np.stack(cents)).cuda())
+    stats = torch.zeros(4, dtype=torch.int32, device="cuda")
+    idx = dc.encode(torch.from_numpy(x).cuda(), stats=stats).cpu().numpy()
+    want = O.quantize(cents, x)
+    assert (idx != want).sum() == 0, f"{(idx != want).sum()} mismatches; stats={stats.tolist()}"
+    assert stats[1].item() > 0, stats.tolist()   # exact scans ran
+
+
+@pytest.mark.parametrize("m,k,g,d", [(3000, 1024, 16, 1024), (999, 256, 32, 1024), (500, 64, 48, 768)])
+def test_decode_narrow_groups(cuda, m, k, g, d):
+    """Per-float4 decode (groups narrower than 128): equals the CPU gather bytewise."""
+    from paper_2505_19342_b200 import vq
+    rng = np.random.default_rng(m + g)
+    gd = d // g
+    cents = rng.normal(size=(g, k, gd)).astype(np.float32)
+    idx = rng.integers(0, k, size=(m, g)).astype(np.int32)
+    dc = vq.DeviceCodebook(torch.from_numpy(cents).cuda())
+    got = dc.decode(torch.from_numpy(idx).cuda()).cpu().numpy()
+    want = np.concatenate([cents[j][idx[:, j]] for j in range(g)], axis=1)
+    np.testing.assert_array_equal(got, want)
