@@ -14,3 +14,6 @@ timeout 900 ncu --profile-from-start off --set full --clock-control none --impor
    -k regex:'tc_gemm|attention_tcp|vq_finalize|layernorm' -c 9 \
    -o gpurun_out/full_$TAG python scripts/profile_forward.py --iters 1 > gpurun_out/full_$TAG.log 2>&1
 ls gpurun_out | tail -20
+timeout 600 python scripts/bench_ranks.py --config vitb --n 1 2 4 8 > gpurun_out/ranks_$TAG.jsonl 2> gpurun_out/ranks_$TAG.err
+timeout 900 python bench.py --config gpt2s --steps 20 > gpurun_out/b_gpt2s_$TAG.json 2> gpurun_out/b_gpt2s_$TAG.err
+timeout 1200 python bench.py --config gpt2m --steps 10 > gpurun_out/b_gpt2m_$TAG.json 2> gpurun_out/b_gpt2m_$TAG.err
