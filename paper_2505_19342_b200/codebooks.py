@@ -145,6 +145,22 @@ def fit_codebooks(params, xs: np.ndarray, codebook_size: int | None = None,
     return books
 
 
+def initialize_codebooks(params, dataset, task: str, codebook_size: int, groups: int,
+                         seed: int = 0, iterations: int = 25) -> None:
+    """Drop-in for train.initialize_codebooks (train.py:176-189): ``dataset`` is the reference's
+    ``(inputs, labels)`` pair for ``task="classify"`` or its list of token-id sequences for
+    ``task="lm"`` (captured on ``ids[:-1]``, train.py:160-173); per-layer codebooks are fitted
+    on the GPU (fit_codebooks) and attached in place.  The training-side residual statistics
+    the reference also fits (fit_residual_stats, for NAVQ noise) are out of scope."""
+    if task == "classify":
+        xs, mode = np.asarray(dataset[0], dtype=np.float32), "classify"
+    elif task == "lm":
+        xs, mode = np.stack([np.asarray(s)[:-1] for s in dataset]), "lm"
+    else:
+        raise ValueError(f"unknown task {task!r}")
+    fit_codebooks(params, xs, codebook_size, groups, seed=seed, iterations=iterations, mode=mode)
+
+
 def load_codebook_tables(path, params=None) -> list[Codebook]:
     """Codebooks from a centroid archive ``{centroids: fp32 [L, G, K, D/G],
     centroids_sha256}`` — e.g. tests/golden/vitb16_codebooks.npz, the reference's own

@@ -129,3 +129,26 @@ def test_gpu_kmeans_equals_reference_lloyd(cuda):
     b = codebooks.kmeans_init(torch.from_numpy(x).cuda(), 16, 1, seed=1)
     np.testing.assert_array_equal(a.centroids[0], b.centroids[0])
     np.testing.assert_array_equal(a.ema_sums[0], b.ema_sums[0])
+
+
+def test_initialize_codebooks_dropin(cuda):
+    """codebooks.initialize_codebooks keeps the reference's signature (train.py:176-189) for both
+    tasks; on the reference's own toy recipe its tables match the oracle's fit (same seeds, the
+    capture forward differing only by fp32-class rounding)."""
+    import paper_2505_19342_b200 as S
+    kw = dict(layers=2, hidden=64, heads=2, vocab_or_classes=10, max_tokens=17, causal=False,
+              codebook_size=16, groups=2)
+    params = S.init_params(S.ModelConfig(**kw), seed=0)
+    op = O.init_params(O.Config(**kw), seed=0)
+    data = O.make_classify_data(64, 16, 6, seed=0, task_seed=0)
+    S.initialize_codebooks(params, data, "classify", 16, 2, seed=0, iterations=10)
+    O.initialize_codebooks(op, data[0], "classify", seed=0, iterations=10)
+    for b, want in zip(params.blocks, op.codebooks):
+        assert b.codebook.groups == 2 and b.codebook.size == 16
+        for g in range(2):
+            np.testing.assert_allclose(b.codebook.centroids[g], want[g], atol=1e-4)
+    lkw = dict(kw, causal=True, vocab_or_classes=32)
+    lp = S.init_params(S.ModelConfig(**lkw), seed=0)
+    seqs = [np.random.default_rng(i).integers(0, 32, 17) for i in range(4)]
+    S.initialize_codebooks(lp, seqs, "lm", 16, 1, seed=0, iterations=5)
+    assert all(b.codebook is not None and b.codebook.size == 16 for b in lp.blocks)

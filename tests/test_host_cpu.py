@@ -130,3 +130,24 @@ def test_native_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert set(declared) == set(_native.SIGNATURES), "ctypes table out of sync with the header"
     assert lib.astra_abi_version() == _native.ABI_VERSION
+
+
+def test_softmax_perturbation_first_order():
+    """attention.softmax_perturbation_first_order: finite-difference agreement, zero sum and
+    validation as the reference's tests (test_attention.py:165-189)."""
+    from paper_2505_19342_b200.attention import softmax_perturbation_first_order as f
+    from paper_2505_19342_b200.errors import ShapeError
+    rng = np.random.default_rng(0)
+    logits = rng.normal(size=9)
+    alpha = np.exp(logits - logits.max())
+    alpha /= alpha.sum()
+    e = rng.normal(size=9)
+    h = 1e-6
+    up = np.exp(logits + h * e - (logits + h * e).max())
+    up /= up.sum()
+    np.testing.assert_allclose(f(alpha, e), (up - alpha) / h, atol=1e-5)
+    assert abs(f(np.array([0.5, 0.3, 0.2]), np.array([1.0, -2.0, 0.5])).sum()) < 1e-12
+    with pytest.raises(ShapeError):
+        f(np.array([0.5, 0.5]), np.zeros(3))
+    with pytest.raises(ValueError):
+        f(np.array([0.9, 0.3]), np.zeros(2))
