@@ -17,9 +17,11 @@ __global__ void __launch_bounds__(288, 1) k(long long* out, int batches, int mod
   __shared__ uint32_t slot;
   __shared__ uint64_t bar;
   __shared__ int stop;
+  __shared__ unsigned int sm_pass[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3f803f80u;
   if (threadIdx.x == 0) { mbar_init(&bar, 1); stop = 0; fence_barrier_init(); }
+  if (threadIdx.x < 8) sm_pass[threadIdx.x] = 0;
   if (warp == 8) tmem_alloc<512>(&slot);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
@@ -31,7 +33,10 @@ __global__ void __launch_bounds__(288, 1) k(long long* out, int batches, int mod
       const uint32_t v_s = smem_u32(sm), a_s = smem_u32(sm + 65536);
       long long t0 = clock64();
       int nw = 0;
-      for (int b = 0; b < batches; ++b) {
+      if (mode & 512) {   // softmax alone: no MMAs, run the softmax warps for a fixed time
+        while (clock64() - t0 < (long long)batches * 2000) {}
+      }
+      for (int b = 0; (mode & 512) == 0 && b < batches; ++b) {
         if (mode >= 128 && mode < 256) {   // 13 SS MMAs 128 x N x 16, K-major A and B, N = mode - 128
           const int N = mode - 128;
           for (int kk = 0; kk < 13; ++kk)
@@ -71,6 +76,7 @@ __global__ void __launch_bounds__(288, 1) k(long long* out, int batches, int mod
       }
       long long t1 = clock64();
       out[blockIdx.x] = (t1 - t0) / batches;
+      if (blockIdx.x == 0) out[3000] = t1 - t0;
       stop = 1;
     }
   } else if (mode & 1) {
@@ -95,8 +101,10 @@ __global__ void __launch_bounds__(288, 1) k(long long* out, int batches, int mod
         tmem_st16(t + g * 16, pk);
       }
       tmem_st_wait();
+      if ((threadIdx.x & 31) == 0) ++sm_pass[warp];
     }
     if (acc.x == 1.2345f) out[1000 + threadIdx.x] = 1;
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) out[2000 + warp] = sm_pass[warp];
   }
   tc_fence_before();
   __syncthreads();
@@ -129,6 +137,21 @@ int main() {
       long long h;
       cudaMemcpy(&h, o, 8, cudaMemcpyDeviceToHost);
       printf("%-22s %lld cycles per batch\n", xn[i], h);
+    }
+  }
+  {
+    const char* sn[] = {"softmax alone", "softmax + PV TS", "softmax + PV SS MN", "softmax + PV SS Kmaj"};
+    const int sm[] = {512 | 1, 64 | 1, 64 | 2 | 1, 64 | 256 | 2 | 1};
+    for (int i = 0; i < 4; ++i) {
+      k<<<148, 288, smem>>>(o, 2000, sm[i]);
+      cudaDeviceSynchronize();
+      long long h[8], tot;
+      cudaMemcpy(h, o + 2000, 64, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&tot, o + 3000, 8, cudaMemcpyDeviceToHost);
+      double passes = 0;
+      for (int w = 0; w < 8; ++w) passes += h[w];
+      // a pass of the 8 warps (2 per lane quarter, alternating groups) is one 128x224 unit
+      printf("%-22s softmax: %.0f cycles per 128x224 unit\n", sn[i], tot / (passes / 8.0));
     }
   }
   for (int m = 9; m < 13; ++m) {
