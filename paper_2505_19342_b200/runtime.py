@@ -680,8 +680,8 @@ class AstraRuntime:
 
     def _serve(self, batches, out, stage, result):
         """Double-buffered serving loop: the host->device copy of batch i+1 (``stage``) runs on
-        a copy stream while batch i's forward runs; each batch's ``result`` is copied back and
-        synchronised before the next is produced."""
+        a copy stream while batch i's forward runs; each batch's ``result`` is copied back, and
+        the host waits for it only after batch i+1's forward has been enqueued."""
         if len(self.x_slots) < 2:
             try:
                 self.capture(slots=2)
@@ -707,6 +707,8 @@ class AstraRuntime:
 
         if n:
             h2d(0)
+        fetched = [torch.cuda.Event() for _ in range(2)]
+        pending = None   # (host buffer, event) of the previous batch's result
         for i in range(n):
             slot = i % 2
             main.wait_event(copied[slot])
@@ -716,9 +718,17 @@ class AstraRuntime:
                 h2d(i + 1)
             host = out[i] if out is not None else torch.empty(result.shape, dtype=result.dtype,
                                                               pin_memory=True)
-            host.copy_(result, non_blocking=True)
-            main.synchronize()   # the batch's result is on the host
-            results.append(host)
+            host.copy_(result, non_blocking=True)   # stream order: before batch i+1 overwrites it
+            fetched[slot].record(main)
+            # one batch stays queued behind the host: wait for the PREVIOUS batch's result only,
+            # so the next forward is already enqueued while the host takes this one
+            if pending is not None:
+                pending[1].synchronize()
+                results.append(pending[0])
+            pending = (host, fetched[slot])
+        if pending is not None:
+            pending[1].synchronize()
+            results.append(pending[0])
         self.check_errors()
         return results
 

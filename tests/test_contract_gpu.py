@@ -152,3 +152,24 @@ def test_initialize_codebooks_dropin(cuda):
     seqs = [np.random.default_rng(i).integers(0, 32, 17) for i in range(4)]
     S.initialize_codebooks(lp, seqs, "lm", 16, 1, seed=0, iterations=5)
     assert all(b.codebook is not None and b.codebook.size == 16 for b in lp.blocks)
+
+
+def test_classify_stream_matches_batch_forward(cuda):
+    """The serving loop (pinned host batches, one forward queued behind the host) returns, per
+    batch, the logits of the plain forward on that batch."""
+    from paper_2505_19342_b200 import cluster, data, model, vq
+    from paper_2505_19342_b200.runtime import AstraRuntime
+    kw = dict(layers=2, hidden=128, heads=2, vocab_or_classes=10, max_tokens=33, causal=False,
+              codebook_size=64, groups=1)
+    params = model.init_params(model.ModelConfig(**kw), seed=0)
+    rng = np.random.default_rng(0)
+    for i, b in enumerate(params.blocks):
+        b.codebook = vq.Codebook(layer_id=i, groups=1,
+                                 centroids=[rng.normal(size=(64, 128)).astype(np.float32)])
+    rt = AstraRuntime(params, cluster.partition_tokens(32, 2), batch=3, precision="parity")
+    batches = [data.make_classify_batch(128, 32, 3, seed=s) for s in range(5)]
+    want = [rt.classify_numpy(b).copy() for b in batches]
+    got = rt.classify_stream([torch.from_numpy(b).pin_memory() for b in batches])
+    assert len(got) == 5
+    for g, w in zip(got, want):
+        np.testing.assert_array_equal(g.numpy(), w)
