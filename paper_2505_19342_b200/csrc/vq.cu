@@ -284,113 +284,6 @@ __device__ __forceinline__ void vq_decide(const AstraCodebook& cb, const float* 
                                           int32_t* __restrict__ idx_out, int32_t* __restrict__ stats,
                                           bool inline_rr, int lane);
 
-// Records epilogue (G = 1 over all 148 SMs; a row's codes span several tiles on different CTA
-// pairs): per (row, 64-code part) the window's upper bound, min lower bound and up to kVqCap
-// candidates; vq_finalize_kernel merges them.  (Finalizing inside the GEMM — the CTA completing
-// a row block decides its rows — measured 141 us vs 52 + 7: the latency-bound decisions land
-// on a few CTAs' critical paths.)
-template <int BN>
-struct VqEpilogue {
-  static constexpr bool kStateful = false;
-  struct State {};
-  int M, K, nchunk;         // nchunk = records per (g, row): kEpiParts per BN-code tile
-  const float4* c_win;      // [G, K] {||c||^2, ||c||, eps ||c||^2, 0}
-  VqWorkspace w;
-
-  __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
-                                             int cb, int ce, int part, uint8_t* stage) const {
-    const int row = tc.m_blk * kBM + row_in_tile;
-    const bool ok = row < M;
-    const int g = tc.batch;
-    const int col_base = tc.n_blk * BN;
-    const float4* cw = c_win + (size_t)g * K;
-    // window terms of the 32 columns of a chunk: one coalesced 16-byte load per lane,
-    // broadcast from smem (columns >= K get ||c||^2 = +inf: never a candidate, U unaffected)
-    float4* scs = reinterpret_cast<float4*>(stage);
-    const int lane = threadIdx.x & 31;
-    // the re-rank list count for the finalize kernel that follows (stream order): reset by
-    // one thread here instead of a memset node in front of this GEMM
-    if (tc.m_blk == 0 && tc.n_blk == 0 && g == 0 && row_in_tile == 0 && cb == 0) {
-      *w.rr_count = 0;
-      w.ov_count[0] = 0;   // (no overflow list in records mode)
-    }
-    const float xn = ok ? w.x_norm[(size_t)g * M + row] : 0.f;
-    const float a = window_a(xn);
-    // pass 1: U = min_j (s_j + D_j)
-    float ub[2] = {INFINITY, INFINITY};
-#pragma unroll 1
-    for (int c0 = cb; c0 < ce; c0 += 32) {
-      const int col0 = col_base + c0;
-      const float4 cl = (col0 + lane < K) ? __ldg(cw + col0 + lane)
-                                          : make_float4(INFINITY, 0.f, 0.f, 0.f);
-      uint32_t r[32];
-      tmem_ld32(taddr + c0, r);
-      tmem_ld_wait();
-      scs[lane] = cl;
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float4 q = scs[j];
-        const float sc = fmaf(-2.0f, __uint_as_float(r[j]), q.x);
-        ub[j & 1] = fminf(ub[j & 1], sc + fmaf(a, q.y, q.z));
-      }
-      __syncwarp();
-    }
-    const float U = fminf(ub[0], ub[1]) + 1e-30f;
-    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk * kEpiParts + part;
-    // pass 2: candidates L_k = s_k - D_k <= U (the chunk's own U; the finalize applies the
-    // global one), and the chunk's min L
-    int cnt = 0;
-    float lmin = INFINITY;
-#pragma unroll 1
-    for (int c0 = cb; c0 < ce; c0 += 32) {
-      const int col0 = col_base + c0;
-      const float4 cl = (col0 + lane < K) ? __ldg(cw + col0 + lane)
-                                          : make_float4(INFINITY, 0.f, 0.f, 0.f);
-      uint32_t r[32];
-      tmem_ld32(taddr + c0, r);
-      tmem_ld_wait();
-      scs[lane] = cl;
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float4 q = scs[j];
-        const float lo = fmaf(-2.0f, __uint_as_float(r[j]), q.x) - fmaf(a, q.y, q.z);
-        lmin = fminf(lmin, lo);
-        if (lo <= U && col0 + j < K) {
-          if (ok && cnt < kVqCap) {
-            w.rec_idx[rec * kVqCap + cnt] = col0 + j;
-            w.rec_score[rec * kVqCap + cnt] = lo;
-          }
-          ++cnt;
-        }
-      }
-      __syncwarp();
-    }
-    if (ok) {
-      w.rec_best[rec] = U;
-      w.rec_lmin[rec] = lmin;
-      w.rec_cnt[rec] = cnt;
-    }
-  }
-
-};
-
-// Grouped codebooks (G > 1): the GEMM runs in "runs" (TileSched::runs) — a CTA pair takes a
-// 128-row block of one group and sweeps every code tile of it — and this epilogue keeps each
-// (row, column part)'s window state in registers across the sweep, then merges the four parts
-// of the row through shared memory and DECIDES the row: one surviving candidate is written as
-// the index; several go to the fp64 re-rank list.  No per-chunk records, no finalize pass
-// (G = 16 at ViT-L: 16 records x 40 B per token-group were 190 MB of HBM traffic per layer).
-constexpr int kRunCap = 4;
-struct VqRunState {
-  float a, dmax2;   // the row's window slope (2 tau + 2 eps) ||x_g|| and 2 Dmax (run constants)
-  float U;       // min (s_k + D_k) over the codes examined in detail (only decreases)
-  float smin;    // min score s_k over every code swept so far
-  float ovl;     // smallest lower bound of a candidate dropped for want of a slot (+inf: none)
-  int n;         // live candidate slots (kept in the warp's stage smem, [slot][lane])
-};
-
 __device__ __forceinline__ void sts_f32(uint32_t a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
 }
@@ -417,6 +310,168 @@ __device__ __forceinline__ void sts_v4(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w) : "memory");
 }
+// Records epilogue (G = 1 over all 148 SMs; a row's codes span several tiles on different CTA
+// pairs): per (row, 64-code part) the window's upper bound, min lower bound and up to kVqCap
+// candidates; vq_finalize_kernel merges them.  (Finalizing inside the GEMM — the CTA completing
+// a row block decides its rows — measured 141 us vs 52 + 7: the latency-bound decisions land
+// on a few CTAs' critical paths.)
+template <int BN>
+struct VqEpilogue {
+  static constexpr bool kStateful = true;
+  static constexpr int kPartCols = BN / kEpiParts;   // 64 (BN 256) or 32 (BN 128)
+  static constexpr int kCh = kPartCols / 32;
+  struct State {
+    float a;   // the row's window slope (2 tau + 2 eps) ||x||
+  };
+  int M, K, nchunk;         // nchunk = records per (g, row): kEpiParts per BN-code tile
+  const float4* c_win;      // [G, K] {||c||^2, ||c||, eps ||c||^2, 0}
+  VqWorkspace w;
+
+  // While the MMAs run: the part's window terms into smem, SoA [0, 256) ||c||^2,
+  // [256, 512) ||c||, [512, 768) -eps ||c||^2, [768, 1024) eps ||c||^2 (columns >= K:
+  // ||c||^2 = +inf, never a candidate, U unaffected), and the row's window slope.
+  __device__ __forceinline__ void pre(const TileCoord& tc, int row_in_tile, int cb, int ce,
+                                      int part, uint8_t* stage, State& st, bool) const {
+    const int lane = threadIdx.x & 31;
+    const int g = tc.batch;
+    const int col0 = tc.n_blk * BN + cb + lane;
+    const float4* cw = c_win + (size_t)g * K;
+    const float4 inf4 = make_float4(INFINITY, 0.f, 0.f, 0.f);
+    const float4 c0 = col0 < K ? __ldg(cw + col0) : inf4;
+    const float4 c1 = (kCh > 1 && col0 + 32 < K) ? __ldg(cw + col0 + 32) : inf4;
+    const int row = tc.m_blk * kBM + row_in_tile;
+    st.a = window_a(row < M ? w.x_norm[(size_t)g * M + row] : 0.f);
+    const uint32_t s_scs = smem_u32(stage);
+    __syncwarp();   // the previous tile's reads of the staged terms are done
+    sts_f32(s_scs + 4 * lane, c0.x);
+    sts_f32(s_scs + 256 + 4 * lane, c0.y);
+    sts_f32(s_scs + 512 + 4 * lane, -c0.z);
+    sts_f32(s_scs + 768 + 4 * lane, c0.z);
+    if (kCh > 1) {
+      sts_f32(s_scs + 128 + 4 * lane, c1.x);
+      sts_f32(s_scs + 384 + 4 * lane, c1.y);
+      sts_f32(s_scs + 640 + 4 * lane, -c1.z);
+      sts_f32(s_scs + 896 + 4 * lane, c1.z);
+    }
+    __syncwarp();
+  }
+
+  // One TMEM read of the part; s_j = ||c_j||^2 - 2 x.c_j, U = min_j (s_j + D_j), candidates
+  // L_j = s_j - D_j <= U (the part's own U; the finalize applies the global one) in code
+  // order, and the part's min L — every expression the same single-rounding FMA/add as the
+  // scalar form, in packed pairs (FFMA2 / FADD2).
+  __device__ __forceinline__ void operator()(const TileCoord& tc, int row_in_tile, uint32_t taddr,
+                                             int cb, int ce, int part, uint8_t* stage, State& st,
+                                             bool, bool) const {
+    const int row = tc.m_blk * kBM + row_in_tile;
+    const bool ok = row < M;
+    const int g = tc.batch;
+    // the re-rank list count for the finalize kernel that follows (stream order): reset by
+    // one thread here instead of a memset node in front of this GEMM
+    if (tc.m_blk == 0 && tc.n_blk == 0 && g == 0 && row_in_tile == 0 && cb == 0) {
+      *w.rr_count = 0;
+      w.ov_count[0] = 0;   // (no overflow list in records mode)
+    }
+    const uint32_t s_scs = smem_u32(stage);
+    const float a = st.a;
+    // s_j of a 32-code chunk from a fresh TMEM read (two reads per chunk keep the epilogue
+    // inside the kernel's 96-register budget)
+    auto scores = [&](int c, float (&sv)[32]) {
+      uint32_t r[32];
+      tmem_ld32(taddr + cb + 32 * c, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 n2 = lds_v4(s_scs + 128 * c + 16 * q);
+        const int j = 4 * q;
+        const float2 t01 = ffma2(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])),
+                                 make_float2(-2.0f, -2.0f), make_float2(n2.x, n2.y));
+        const float2 t23 = ffma2(make_float2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])),
+                                 make_float2(-2.0f, -2.0f), make_float2(n2.z, n2.w));
+        sv[j] = t01.x;
+        sv[j + 1] = t01.y;
+        sv[j + 2] = t23.x;
+        sv[j + 3] = t23.y;
+      }
+    };
+    // pass 1: U = min_j (s_j + D_j)
+    float u4[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+#pragma unroll 1
+    for (int c = 0; c < kCh; ++c) {
+      float sv[32];
+      scores(c, sv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 nn = lds_v4(s_scs + 256 + 128 * c + 16 * q);
+        const float4 ee = lds_v4(s_scs + 768 + 128 * c + 16 * q);
+        const int j = 4 * q;
+        const float2 u01 = fadd2(make_float2(sv[j], sv[j + 1]),
+                                 ffma2(make_float2(a, a), make_float2(nn.x, nn.y), make_float2(ee.x, ee.y)));
+        const float2 u23 = fadd2(make_float2(sv[j + 2], sv[j + 3]),
+                                 ffma2(make_float2(a, a), make_float2(nn.z, nn.w), make_float2(ee.z, ee.w)));
+        u4[q & 1] = fmin3(u4[q & 1], u01.x, u01.y);
+        u4[2 + (q & 1)] = fmin3(u4[2 + (q & 1)], u23.x, u23.y);
+      }
+    }
+    const float U = fminf(fminf(u4[0], u4[1]), fminf(u4[2], u4[3])) + 1e-30f;
+    const size_t rec = ((size_t)g * M + row) * nchunk + tc.n_blk * kEpiParts + part;
+    const int col0 = tc.n_blk * BN + cb;
+    const int nvalid = K - col0;   // columns j >= nvalid are padding
+    // pass 2: L = s - D = s + (-a ||c|| - eps ||c||^2), candidates in code order
+    int cnt = 0;
+    float l4[2] = {INFINITY, INFINITY};
+#pragma unroll 1
+    for (int c = 0; c < kCh; ++c) {
+      float sv[32];
+      scores(c, sv);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 nn = lds_v4(s_scs + 256 + 128 * c + 16 * q);
+        const float4 ne = lds_v4(s_scs + 512 + 128 * c + 16 * q);
+        const int j = 4 * q;
+        const float2 l01 = fadd2(make_float2(sv[j], sv[j + 1]),
+                                 ffma2(make_float2(-a, -a), make_float2(nn.x, nn.y), make_float2(ne.x, ne.y)));
+        const float2 l23 = fadd2(make_float2(sv[j + 2], sv[j + 3]),
+                                 ffma2(make_float2(-a, -a), make_float2(nn.z, nn.w), make_float2(ne.z, ne.w)));
+        l4[0] = fmin3(l4[0], l01.x, l01.y);
+        l4[1] = fmin3(l4[1], l23.x, l23.y);
+        const float lo[4] = {l01.x, l01.y, l23.x, l23.y};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int jj = 32 * c + j + t;
+          if (lo[t] <= U && jj < nvalid) {
+            if (ok && cnt < kVqCap) {
+              w.rec_idx[rec * kVqCap + cnt] = col0 + jj;
+              w.rec_score[rec * kVqCap + cnt] = lo[t];
+            }
+            ++cnt;
+          }
+        }
+      }
+    }
+    if (ok) {
+      w.rec_best[rec] = U;
+      w.rec_lmin[rec] = fminf(l4[0], l4[1]);
+      w.rec_cnt[rec] = cnt;
+    }
+  }
+};
+
+// Grouped codebooks (G > 1): the GEMM runs in "runs" (TileSched::runs) — a CTA pair takes a
+// 128-row block of one group and sweeps every code tile of it — and this epilogue keeps each
+// (row, column part)'s window state in registers across the sweep, then merges the four parts
+// of the row through shared memory and DECIDES the row: one surviving candidate is written as
+// the index; several go to the fp64 re-rank list.  No per-chunk records, no finalize pass
+// (G = 16 at ViT-L: 16 records x 40 B per token-group were 190 MB of HBM traffic per layer).
+constexpr int kRunCap = 4;
+struct VqRunState {
+  float a, dmax2;   // the row's window slope (2 tau + 2 eps) ||x_g|| and 2 Dmax (run constants)
+  float U;       // min (s_k + D_k) over the codes examined in detail (only decreases)
+  float smin;    // min score s_k over every code swept so far
+  float ovl;     // smallest lower bound of a candidate dropped for want of a slot (+inf: none)
+  int n;         // live candidate slots (kept in the warp's stage smem, [slot][lane])
+};
+
 // r[j] for a run-time j in [0, 32): a 5-level select tree (keeps r in registers)
 __device__ __forceinline__ float pick32(const uint32_t (&r)[32], int j) {
   float t16[16], t8[8], t4[4], t2[2];
@@ -1439,6 +1494,12 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
                             cudaStream_t s, const int32_t* row_tok_in = nullptr) {
   const int G = cb.groups, K = cb.size, gdp = cb.padded_dim;
   if (Mg <= 0 || M <= 0) return ASTRA_OK;   // (the GEMM's tile (0, 0) resets the re-rank count)
+  static int debug_set = -1;
+  if (debug_set < 0) {   // bench-only isolation switch for this unit's GEMMs, see tc_gemm.cuh
+    const char* d = getenv("ASTRA_VQ_GEMM_DEBUG");
+    debug_set = d ? atoi(d) : 0;
+    if (debug_set) ASTRA_CUDA_CHECK(cudaMemcpyToSymbol(g_gemm_debug, &debug_set, sizeof(int)));
+  }
   const int cluster = (Mg > kBM) ? 2 : 1;  // CTA pairs split the codebook tile (cta_group::2)
   const long units256 = (long)G * ((Mg + kBM * cluster - 1) / (kBM * cluster)) * ((K + kVqBN - 1) / kVqBN);
   const int bn = (units256 * 2 * cluster <= num_sms()) ? kVqBNMin : kVqBN;
