@@ -877,6 +877,88 @@ __global__ void vq_finalize_kernel(AstraCodebook cb, const float* __restrict__ x
             lane);
 }
 
+// vq_finalize for <= 16 records per row (K <= 1024 at BN = 256): two rows per warp, a
+// half-warp per row, so every lane carries a record and the grid is one resident wave at
+// ViT-B (the per-row work is one round trip of record loads; a full warp per row left half
+// the lanes idle and needed 1.3 waves).  Same decisions as vq_decide without inline re-rank:
+// one surviving candidate is the index, several (or an overflowed part) go to the re-rank
+// list, the candidate codes compacted in code order when they fit.
+__global__ void vq_finalize_half_kernel(AstraCodebook cb, int M, const int32_t* __restrict__ rows,
+                                        VqWorkspace w, int nchunk, int32_t* __restrict__ idx_out,
+                                        int32_t* __restrict__ stats, int Mrec, int rec_by_row) {
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, hl = lane & 15, lead = lane & 16;
+  const int G = cb.groups;
+  const int item = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 2 + (lane >> 4);
+  const bool on = item < G * M;
+  const int g = on ? item / M : 0, row = on ? item - g * M : 0;
+  const bool has = on && hl < nchunk;
+  float rb = INFINITY, rl = INFINITY, sc[kVqCap];
+  int rc = 0, ix[kVqCap];
+  if (has) {
+    const int rr = rec_by_row ? rows[row] : row;
+    const size_t rec = ((size_t)g * Mrec + rr) * nchunk + hl;
+    rb = w.rec_best[rec];
+    rl = w.rec_lmin[rec];
+    rc = w.rec_cnt[rec];
+#pragma unroll
+    for (int i = 0; i < kVqCap; ++i) {
+      sc[i] = w.rec_score[rec * kVqCap + i];
+      ix[i] = w.rec_idx[rec * kVqCap + i];
+    }
+  }
+  float best = rb;
+#pragma unroll
+  for (int o = 8; o; o >>= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
+  int n = 0, only = 0x7FFFFFFF, overflow = 0;
+  uint32_t live = 0;
+  if (has && rl <= best) {
+    overflow = rc > kVqCap;
+#pragma unroll
+    for (int i = 0; i < kVqCap; ++i)
+      if (i < rc && sc[i] <= best) {
+        ++n;
+        only = min(only, ix[i]);
+        live |= 1u << i;
+      }
+  }
+  int pre = __popc(live);
+  const int mine = pre;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, pre, o, 16);
+    if (hl >= o) pre += t;
+  }
+  pre -= mine;
+#pragma unroll
+  for (int o = 8; o; o >>= 1) {
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+    only = min(only, __shfl_xor_sync(0xffffffffu, only, o));
+    overflow |= __shfl_xor_sync(0xffffffffu, overflow, o);
+  }
+  const bool rr = on && (overflow || n > 1);
+  int slot = 0;
+  if (rr && hl == 0) slot = atomicAdd(w.rr_count, 1);
+  slot = __shfl_sync(0xffffffffu, slot, lead);
+  if (rr) {
+    int* ent = w.rr_list + (size_t)slot * kRREntry;
+    const bool direct = !overflow && n <= kRRCands;
+    if (direct) {
+#pragma unroll
+      for (int i = 0; i < kVqCap; ++i)
+        if ((live >> i) & 1u) ent[2 + pre++] = ix[i];
+    }
+    if (hl == 0) {
+      ent[0] = item;
+      ent[1] = direct ? n : -1;
+    }
+  } else if (on && hl == 0) {
+    idx_out[(size_t)row * G + g] = only;
+  }
+  if (on && hl == 0 && stats) atomicAdd(&stats[2], n);
+}
+
 // Exact fp64 re-rank of the listed items (one warp per item, grid-stride over the list): the
 // window's candidate codes are compacted into a per-warp list and each is scored with the
 // reference expression (||p||^2 - 2 p.c) + ||c||^2 (vq.py:130), ties to the lowest index.
@@ -1553,8 +1635,12 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
                                     : vq_launch_gemm<kVqBNMin>(cb, ta, talo, Mg, w, nchunk, cluster, s);
   ASTRA_CUDA_CHECK(e);
   const int items = G * M;
-  launch_k(vq_finalize_kernel, (items + 7) / 8, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
-                                                      stats, Mg, rec_by_row);
+  if (nchunk <= 16)
+    launch_k(vq_finalize_half_kernel, (items + 15) / 16, 256, 0, s, cb, M, rows, w, nchunk, idx_out,
+                                                             stats, Mg, rec_by_row);
+  else
+    launch_k(vq_finalize_kernel, (items + 7) / 8, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
+                                                        stats, Mg, rec_by_row);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   launch_k(vq_rerank_kernel<false>, num_sms() * 4, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
                                                  Mg, rec_by_row, bn / kEpiParts);
