@@ -16,6 +16,7 @@
 // in padded shared memory).  It is exact enough for the fp32 parity mode and general in T.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -506,6 +507,7 @@ constexpr int kPSmem = kPSmemUsed + 1024;
 
 // Debug timeline (astra_attention_trace): CTA 0 records globaltimer stamps per chunk.
 __device__ long long* g_attn_trace = nullptr;
+__device__ int g_attn_pipe_delay = 0;   // ns: pipeline 1 starts this late (ASTRA_ATTN_PIPE_DELAY)
 __device__ __forceinline__ void p_trace(long long* tr, int slot, uint32_t u) {
   if (tr != nullptr && u < 32) {
     long long t;
@@ -653,6 +655,7 @@ __device__ __forceinline__ void p_producer(const AttnArgs& a, const PMaps& mp, i
                                            int* kpos2, PBars* b, int lane, long long* trace) {
   PIter it;
   it.init(a, qtiles, pipe, items, n_items);
+  if (pipe == 1 && g_attn_pipe_delay > 0) __nanosleep(g_attn_pipe_delay);
   for (uint32_t n = 0; it.cur.ok; ++n, it.advance(a)) {
     const PUnit un = it.cur;
     const uint32_t ph = n & 1;
@@ -1854,6 +1857,12 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
       configured = true;
     }
     const int qtiles = (max_nq + kTQ - 1) / kTQ;
+    static int delay_set = -1;
+    if (delay_set < 0) {   // bench-only experiment switch (default 0: both pipelines start at once)
+      const char* d = getenv("ASTRA_ATTN_PIPE_DELAY");
+      delay_set = d ? atoi(d) : 0;
+      if (delay_set) ASTRA_CUDA_CHECK(cudaMemcpyToSymbol(g_attn_pipe_delay, &delay_set, sizeof(int)));
+    }
     if (g_attention_variant != 1) {
       const long items = (long)num_segs * heads * qtiles;
       const int grid = (int)std::min<long>(items, num_sms());

@@ -7,7 +7,7 @@
               rank of an N-way split (loopback exchange), back-to-back launches; algorithmic
               Q/K/V read + O write bytes against the measured HBM copy bandwidth
 
-    python scripts/microbench.py [--reps 30]
+    python scripts/microbench.py [--reps 30] [--only vq|attention]
 """
 import argparse
 import json
@@ -111,11 +111,14 @@ def attention_cases(reps, peaks, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=30)
+    ap.add_argument("--only", choices=["vq", "attention"], default=None)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     peaks = bench._peaks()
-    vq_cases(a.reps, peaks, dev)
-    attention_cases(a.reps, peaks, dev)
+    if a.only != "attention":
+        vq_cases(a.reps, peaks, dev)
+    if a.only != "vq":
+        attention_cases(a.reps, peaks, dev)
 
 
 if __name__ == "__main__":
