@@ -965,6 +965,12 @@ __global__ void vq_finalize_half_kernel(AstraCodebook cb, int M, const int32_t* 
 // For group widths <= 1024 each lane loads its slice of the token and of a candidate row in
 // one batch of independent loads (one memory round trip per candidate, not one per 32
 // elements); a chunk whose candidate list overflowed contributes all of its 64 codes.
+// Grid (blocks per SM): the generic variant's 239 registers fit one 256-thread block per SM,
+// and its G = 1 lists are short (~560 items per ViT-B layer, one per warp), so the grid is the
+// co-resident blocks (4 per SM spent ~1 us retiring empty blocks one at a time: 4.4 -> 3.3 us).
+// The narrow variant serves the long grouped-codebook lists, where queued blocks balance the
+// statically strided items better (G = 32 with 2 per SM: 430 -> 483 us).
+constexpr int kRerankBlocks = 1, kRerankBlocksNarrow = 8;
 template <bool kNarrow>
 __global__ void __launch_bounds__(256) vq_rerank_kernel(AstraCodebook cb, const float* __restrict__ x,
                                                         int M, int ldx,
@@ -1623,10 +1629,10 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
     ASTRA_CUDA_CHECK(er);
     const int gd = cb.group_dim;
     if (gd <= 128 && gd % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0)
-      launch_k(vq_rerank_kernel<true>, num_sms() * 8, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
+      launch_k(vq_rerank_kernel<true>, num_sms() * kRerankBlocksNarrow, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                            stats, Mg, rec_by_row, bn / kEpiParts);
     else
-      launch_k(vq_rerank_kernel<false>, num_sms() * 4, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
+      launch_k(vq_rerank_kernel<false>, num_sms() * kRerankBlocks, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                             stats, Mg, rec_by_row, bn / kEpiParts);
     ASTRA_CUDA_CHECK(cudaGetLastError());
     return ASTRA_OK;
@@ -1642,7 +1648,7 @@ static int vq_gemm_finalize(const AstraCodebook& cb, const void* a_hi, const voi
     launch_k(vq_finalize_kernel, (items + 7) / 8, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out,
                                                         stats, Mg, rec_by_row);
   ASTRA_CUDA_CHECK(cudaGetLastError());
-  launch_k(vq_rerank_kernel<false>, num_sms() * 4, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
+  launch_k(vq_rerank_kernel<false>, num_sms() * kRerankBlocks, 256, 0, s, cb, x, M, ldx, rows, w, nchunk, idx_out, stats,
                                                  Mg, rec_by_row, bn / kEpiParts);
   ASTRA_CUDA_CHECK(cudaGetLastError());
   return ASTRA_OK;

@@ -30,6 +30,8 @@ def window_stats(x, c):
         cand = (d - win <= best[:, None] + dbest).sum(1).double()
         out[name] = {"cands_per_token": round(cand.mean().item(), 4),
                      "multi_rate": round((cand > 1).double().mean().item(), 5),
+                     "max_cands": int(cand.max().item()), "over8": int((cand > 8).sum().item()),
+                     "over4": int((cand > 4).sum().item()),
                      "xnorm": round(xn.mean().item(), 3), "cnorm": round(cn.mean().item(), 3)}
     dup = (torch.cdist(c, c) == 0).sum().item() - c.shape[0]
     out["duplicate_code_pairs"] = dup // 2
@@ -63,7 +65,9 @@ def main():
         for g in range(w.G):
             c = torch.from_numpy(np.asarray(cb.centroids[g], np.float64)).to(dev)
             per.append(window_stats(x[:, g * gd:(g + 1) * gd], c))
-        agg = {k: {kk: float(np.mean([p[k][kk] for p in per])) for kk in per[0][k]}
+        agg = {k: {kk: (float(np.max([p[k][kk] for p in per])) if kk == "max_cands" else
+                        float(np.sum([p[k][kk] for p in per])) if kk.startswith("over") else
+                        float(np.mean([p[k][kk] for p in per]))) for kk in per[0][k]}
                for k in ("raw", "centred")}
         agg["duplicate_code_pairs"] = int(sum(p["duplicate_code_pairs"] for p in per))
         agg["gap12_median"] = float(np.mean([p["gap12_median"] for p in per]))
