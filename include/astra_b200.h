@@ -254,6 +254,10 @@ int astra_attention_force_simt(int enable);
 /* Test hook: tcgen05 variant — 0 persistent two-pipeline (default), 1 one CTA per tile,
    2 persistent single pipeline with correction warps (attention_tcs_kernel). */
 int astra_attention_variant(int variant);
+/* Programmatic-dependent-launch policy for this host thread's subsequent launches: 0 none,
+   1 every kernel, 2 persistent kernels only (default), -1 back to ASTRA_PDL / the default.
+   Returns the previous override (-1: none). */
+int astra_pdl_override(int mode);
 /* Debug hook: CTA 0 of the persistent kernel writes per-unit globaltimer stamps
  * (int64 [64][8]) to buf; NULL disables. */
 int astra_attention_trace(void* buf);

@@ -55,6 +55,7 @@ SIGNATURES: dict[str, list] = {
                         _c_int, _c_int, _c_int, _c_int, _vp],
     "astra_attention_force_simt": [_c_int],
     "astra_attention_variant": [_c_int],
+    "astra_pdl_override": [_c_int],
     "astra_attention_trace": [_vp],
     "astra_gather_kv": [_vp, _c_int, _c_int, _c_int, _vp, _vp, _c_int, _vp, _vp, _c_int, _c_int,
                         _vp, _c_int, _vp],

@@ -15,12 +15,20 @@ void set_last_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+static thread_local int g_pdl_override = -1;   // astra_pdl_override (this host thread's launches)
+
 int pdl_mode() {
   static const int mode = [] {
     const char* e = getenv("ASTRA_PDL");
     return e && e[0] >= '0' && e[0] <= '2' ? e[0] - '0' : 2;
   }();
-  return mode;
+  return g_pdl_override >= 0 ? g_pdl_override : mode;
+}
+
+int set_pdl_override(int mode) {
+  const int prev = g_pdl_override;
+  g_pdl_override = mode >= 0 && mode <= 2 ? mode : -1;
+  return prev;
 }
 
 int num_sms() {
@@ -76,3 +84,8 @@ int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, 
 extern "C" const char* astra_last_error(void) { return astra::g_last_error; }
 
 extern "C" int astra_abi_version(void) { return ASTRA_ABI_VERSION; }
+
+// Programmatic-dependent-launch policy for the calling host thread's subsequent launches
+// (0 none, 1 every kernel, 2 persistent kernels only, -1 back to ASTRA_PDL / the default).
+// The runtime turns it off around the Q|K|V GEMM when the VQ chain is on the critical path.
+extern "C" int astra_pdl_override(int mode) { return astra::set_pdl_override(mode); }

@@ -46,6 +46,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Programmatic dependent launch: ASTRA_PDL=0 off, 1 every kernel, 2 (default) only the
 // persistent tensor-core kernels (GEMM, attention) — see DESIGN §3.5.
 int pdl_mode();
+int set_pdl_override(int mode);   // -1: back to ASTRA_PDL / the default; returns the previous
 inline bool pdl_enabled() { return pdl_mode() == 1; }
 inline bool pdl_persistent() { return pdl_mode() >= 1; }
 

@@ -27,6 +27,7 @@ from __future__ import annotations
 import contextlib
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
@@ -166,6 +167,7 @@ class AstraRuntime:
         # the VQ / exchange branch is on the critical path at N > 1: high stream priority
         self.side_stream = torch.cuda.Stream(device=self.device, priority=-1)
         self.overlap_vq = True   # False: strictly sequential launches (isolated kernel timing)
+        self.qkv_after_vq = os.environ.get("ASTRA_QKV_PDL", "0") != "1"
         self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
         self.graph = None
         self.graphs = []
@@ -463,12 +465,20 @@ class AstraRuntime:
             self.trace.append(self.idx_all.clone())
         elif self.trace is not None:
             self.trace.append(self.idx_all.clone())
-        # 4. fused Q|K|V projection
+        # 4. fused Q|K|V projection.  With remote keys the VQ chain, not this GEMM, gates the
+        #    attention: launched without programmatic early start, the GEMM's persistent CTAs do
+        #    not occupy the SMs before LN1 ends, and the (high-priority) VQ GEMM goes first.
         whi, wlo = lay["wqkv"]
-        with self._op("gemm_qkv"):
-            kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo,
-                         out_f32=None if self.fast else self.qkv,
-                         out_hi=self.qkv if self.fast else None)
+        late = side_work and self.has_remote and self.qkv_after_vq
+        prev = _native.load().astra_pdl_override(0) if late else None
+        try:
+            with self._op("gemm_qkv"):
+                kernels.gemm(self.ln_hi, whi, a_lo=self.ln_lo, b_lo=wlo,
+                             out_f32=None if self.fast else self.qkv,
+                             out_hi=self.qkv if self.fast else None)
+        finally:
+            if late:
+                _native.load().astra_pdl_override(prev)
         joined = not side_work or self.trace is not None
         self._layer_rest(l, lay, remote, join_before_attn=not joined and self.has_remote,
                          join_before_w2=not joined and not self.has_remote)
