@@ -590,9 +590,17 @@ struct VqRunEpilogue {
       // + a rounding margin of 2^-21 (|smin| + 2 Dmax): the comparisons stay exact supersets
       const float thr = (st.smin + dmax2) + kEps * (fabsf(st.smin) + dmax2);
       if (cmin > thr) continue;   // common case: nothing in this chunk can compete
+      // bit j = (s_j <= thr) = sign of s_j - thr' (thr' the next float above thr; the difference
+      // of finite floats is exact in sign, +inf scores give +inf), packed pairwise and shifted
+      // in with one funnel shift per code
+      const float2 nthr = make_float2(-nextafterf(thr, INFINITY), -nextafterf(thr, INFINITY));
       uint32_t m = 0;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) m |= (__uint_as_float(r[j]) <= thr ? 1u : 0u) << j;
+      for (int j = 30; j >= 0; j -= 2) {
+        const float2 dd = fadd2(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), nthr);
+        m = __funnelshift_l(__float_as_uint(dd.y), m, 1);
+        m = __funnelshift_l(__float_as_uint(dd.x), m, 1);
+      }
       while (m) {
         const int j = __ffs(m) - 1;
         m &= m - 1;
