@@ -1515,7 +1515,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
 // 64-127 -> cols 64-95), Pl at [128,192), O at [192,256).
 constexpr int kT3Q = 128, kT3KC = 128, kT3Threads = 256;
 constexpr int kT3Tile = 16384;   // 128 rows x 64 bf16, SW128
-constexpr int kT3SmemUsed = 6 * kT3Tile + 256 + 4 * 128 * 4 + 64;
+constexpr int kT3SmemUsed = 6 * kT3Tile + 2 * 128 * 2 + 2 * 128 * 4 + 4 * 128 * 4 + 64;
 constexpr int kT3Smem = kT3SmemUsed + 1024;
 
 // 8 fp32 values -> bf16 hi and lo 16-byte chunks at chunk c of row r of two SW128 tiles.
@@ -1554,12 +1554,15 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
   uint8_t* sKl = sm + 3 * kT3Tile;
   uint8_t* sVh = sm + 4 * kT3Tile;
   uint8_t* sVl = sm + 5 * kT3Tile;
-  short* sKpos = reinterpret_cast<short*>(sm + 6 * kT3Tile);
-  float* sRed = reinterpret_cast<float*>(sm + 6 * kT3Tile + 256);   // [max|sum][half][128]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * kT3Tile + 256 + 2048);
+  short* sKposB = reinterpret_cast<short*>(sm + 6 * kT3Tile);        // [2][128] key positions
+  int* sSrc = reinterpret_cast<int*>(sm + 6 * kT3Tile + 512);         // [2][128] key sources
+  float* sRed = reinterpret_cast<float*>(sm + 6 * kT3Tile + 1536);   // [max|sum][half][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * kT3Tile + 1536 + 2048);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
 
-  const int seg = blockIdx.x, h = blockIdx.y, qt = blockIdx.z;
+  // query tile fastest: the tiles of one (segment, head) run together and share its K/V rows
+  // through L2 instead of re-reading them a wave later
+  const int qt = blockIdx.x, seg = blockIdx.y, h = blockIdx.z;
   const int* sg = a.segs + seg * 6;
   const int q0 = sg[0], nq = sg[1], qpos0 = sg[2], ncontent = sg[3], k0 = sg[4], nk = sg[5];
   if (qt * kT3Q >= nq) return;
@@ -1571,6 +1574,11 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_barrier_init();
+  }
+  if (tid < kT3KC) {   // first chunk's key sources / positions (published by the barrier below)
+    const bool in = tid < nk;
+    sSrc[tid] = in ? __ldg(a.key_src + k0 + tid) : 0;
+    sKposB[tid] = in ? (a.causal ? (short)__ldg(a.key_pos + k0 + tid) : (short)0) : kPosNever;
   }
   // Q tile: 128 rows x 8 chunks, four (row, chunk) units per thread, loads issued first
   {
@@ -1613,22 +1621,32 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
 
   const int nchunks = (nk + kT3KC - 1) / kT3KC;
   for (int c = 0; c < nchunks; ++c) {
-    const int kc = c * kT3KC;
+    const int kc = c * kT3KC, buf = c & 1;
     const int valid = min(kT3KC, nk - kc);
+    const int* cSrc = sSrc + buf * kT3KC;
+    const short* sKpos = sKposB + buf * kT3KC;
+    // next chunk's key sources / positions: loads issued now, stored into the other buffer at
+    // the end of this chunk (its latency hides behind this chunk's work)
+    int nsrc = 0;
+    short npos = kPosNever;
+    if (tid < kT3KC && kc + kT3KC + tid < nk) {
+      nsrc = __ldg(a.key_src + k0 + kc + kT3KC + tid);
+      npos = a.causal ? (short)__ldg(a.key_pos + k0 + kc + kT3KC + tid) : (short)0;
+    }
     // causal: a chunk none of whose keys is visible to any query of the tile contributes
     // nothing (p = 0 for all of it) and is skipped; replica keys (position -1) stay visible
-    if (a.causal && !__syncthreads_or(tid < valid && (int)__ldg(a.key_pos + k0 + kc + tid) <= qpos_max))
-      continue;
+    const bool run = !a.causal || __syncthreads_or(tid < valid && (int)sKpos[tid] <= qpos_max);
+    if (run) {
     const int ncols = (valid + 15) & ~15;
-    // ---- K and V chunk: 2 x 128 rows x 8 chunks = 2048 units, 8 per thread
+    // ---- K chunk: 128 rows x 8 chunks = 1024 units, 4 per thread; S = Q K^T issued as soon
+    // as K is in place, the V chunk is loaded and split while those MMAs run
     {
-      float4 ka[8], kb[8];
+      float4 ka[4], kb[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int u = tid + i * kT3Threads, mv = u >> 10, r = (u >> 3) & 127, cc = u & 7;
+      for (int i = 0; i < 4; ++i) {
+        const int u = tid + i * kT3Threads, r = u >> 3, cc = u & 7;
         if (r < valid) {
-          const int src = __ldg(a.key_src + k0 + kc + r);
-          const float* p = t3_key_row(a, src, mv != 0, hoff) + cc * 8;
+          const float* p = t3_key_row(a, cSrc[r], false, hoff) + cc * 8;
           ka[i] = __ldg(reinterpret_cast<const float4*>(p));
           kb[i] = __ldg(reinterpret_cast<const float4*>(p + 4));
         } else {
@@ -1636,13 +1654,10 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
         }
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int u = tid + i * kT3Threads, mv = u >> 10, r = (u >> 3) & 127, cc = u & 7;
-        t3_store_split(ka[i], kb[i], mv ? sVh : sKh, mv ? sVl : sKl, r, cc);
+      for (int i = 0; i < 4; ++i) {
+        const int u = tid + i * kT3Threads;
+        t3_store_split(ka[i], kb[i], sKh, sKl, u >> 3, u & 7);
       }
-      if (tid < kT3KC)
-        sKpos[tid] = tid < valid ? (a.causal ? (short)__ldg(a.key_pos + k0 + kc + tid) : (short)0)
-                                 : kPosNever;
     }
     fence_proxy_async();
     tc_fence_before();
@@ -1661,6 +1676,26 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
       }
       umma_commit(bar);
     }
+    {
+      float4 va[4], vb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int u = tid + i * kT3Threads, r = u >> 3, cc = u & 7;
+        if (r < valid) {
+          const float* p = t3_key_row(a, cSrc[r], true, hoff) + cc * 8;
+          va[i] = __ldg(reinterpret_cast<const float4*>(p));
+          vb[i] = __ldg(reinterpret_cast<const float4*>(p + 4));
+        } else {
+          va[i] = vb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int u = tid + i * kT3Threads;
+        t3_store_split(va[i], vb[i], sVh, sVl, u >> 3, u & 7);
+      }
+    }
+    fence_proxy_async();   // V tiles: published to the P.V MMAs by the barrier below
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
@@ -1747,8 +1782,13 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
 #pragma unroll
       for (int d = 0; d < 32; ++d) o[d] = fmaf(o[d], corr, __uint_as_float(r0[d]));
     }
+    }   // run
+    if (tid < kT3KC) {
+      sSrc[(buf ^ 1) * kT3KC + tid] = nsrc;
+      sKposB[(buf ^ 1) * kT3KC + tid] = npos;
+    }
     tc_fence_before();
-    __syncthreads();   // K/V tiles and TMEM columns are free for the next chunk
+    __syncthreads();   // K/V tiles, TMEM columns and the staged key buffer free for the next chunk
   }
 
   sRed[256 + half * 128 + row] = l_half;
@@ -1914,7 +1954,7 @@ extern "C" int astra_attention(const void* q, int ldq, const void* k_local, cons
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kT3Smem));
       configured3 = true;
     }
-    dim3 tgrid(num_segs, heads, (max_nq + kT3Q - 1) / kT3Q);
+    dim3 tgrid((max_nq + kT3Q - 1) / kT3Q, num_segs, heads);
     launch_kp(attention_tc3_kernel, tgrid, kT3Threads, kT3Smem, st, a);
     ASTRA_CUDA_CHECK(cudaGetLastError());
     return ASTRA_OK;
