@@ -1718,7 +1718,8 @@ __global__ void __launch_bounds__(kT3Threads, 2) attention_tc3_kernel(AttnArgs a
       }
     }
     sRed[half * 128 + row] = mx;
-    __syncthreads();
+    // only the two warps sharing these TMEM lanes (quarter, halves 0 and 1) exchange maxima
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
     const float cmax = fmaxf(sRed[row], sRed[128 + row]);
     const float mnew = fmaxf(m_run, cmax);
     const float corr = (m_run == -INFINITY) ? 0.f : expf(m_run - mnew);
