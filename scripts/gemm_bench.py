@@ -31,5 +31,8 @@ for M, N, K in shapes:
     tg = bench(lambda: kernels.gemm(a, b, bias=bias, gelu=2, out_hi=outh))
     res = torch.randn(M, N, device="cuda")
     tr = bench(lambda: kernels.gemm(a, b, bias=bias, residual=res, out_f32=out))
-    print(f"   +bias+gelu->bf16 {tg*1e6:.1f}us | +bias+residual->f32 {tr*1e6:.1f}us", flush=True)
+    # the same fused outputs from cuBLAS + torch elementwise ops (what an unfused path launches)
+    tcg = bench(lambda: torch.nn.functional.gelu(torch.addmm(bias.to(torch.bfloat16), a, b.T)))
+    tcr = bench(lambda: torch.add(torch.matmul(a, b.T).float(), res).add_(bias))
+    print(f"   +bias+gelu->bf16 {tg*1e6:.1f}us (cublas+torch {tcg*1e6:.1f}us) | +bias+residual->f32 {tr*1e6:.1f}us (cublas+torch {tcr*1e6:.1f}us)", flush=True)
     print(f"{M}x{N}x{K}: bf16 {t1*1e6:.1f}us {fl/t1/1e12:.0f} TF/s | bf16x3 {t3*1e6:.1f}us {3*fl/t3/1e12:.0f} TF/s(eff x3) | cublas {tc*1e6:.1f}us {fl/tc/1e12:.0f} TF/s", flush=True)
